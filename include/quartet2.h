@@ -1,0 +1,144 @@
+/*
+ * quartet2.h — C ABI of the B200-native Quartet II NVFP4 linear-layer kernels.
+ *
+ * The reference (nvfp4emu, /root/reference/pkg/src/nvfp4emu) has no FFI: its
+ * boundary is a pure-Python function API.  Each entry point below replaces one
+ * of those functions (cited per declaration); the Python package
+ * paper_2601_22813_b200 binds them with ctypes and keeps the reference's names,
+ * argument meanings and exceptions.  See INTEGRATION.md for the binding.
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers; every call is stream-ordered on
+ *    `stream` (a cudaStream_t passed as void*), asynchronous, and allocates
+ *    nothing.  Callers own every buffer.
+ *  - Return value: Q2_OK, Q2_EINVAL (bad shape / argument; nothing launched)
+ *    or Q2_ECUDA (launch error).
+ *  - Data-dependent failures that the reference raises as ValueError /
+ *    OverflowError are OR-ed into the device word `err` (Q2_ERR_* bits); the
+ *    host wrapper reads it and raises with the reference's message.
+ *  - Reentrant: no global mutable state.  Concurrent calls are safe on
+ *    distinct streams with distinct workspaces.
+ *
+ * NVFP4 tensor in HBM (q2_nvfp4): a logical [R, K] tensor quantized along K.
+ *  codes   uint8 [R, K/2], row-major, two E2M1 codes per byte, low nibble =
+ *          even k (the NV4T packing of quantizers.py:339).
+ *  sf      UE4M3 group scales (one per 16 along K) in the tcgen05 block-scale
+ *          atom layout: 512-byte atoms of 128 rows x 4 scales, atoms K-fastest,
+ *          rows padded to a multiple of 128 with zero scales.  Byte of (r, j):
+ *            ((r/128)*ceil(K/64) + j/4)*512 + (r%32)*16 + ((r%128)/32)*4 + j%4
+ *          Size: q2_sf_bytes(R, K).
+ *  scale32 float32 device scalar (the reference's np.float32 tensor scale).
+ */
+#ifndef QUARTET2_H_
+#define QUARTET2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { Q2_OK = 0, Q2_EINVAL = 1, Q2_ECUDA = 2 };
+enum { Q2_BF16 = 0, Q2_F32 = 1 };
+
+/* err-word bits (device uint32) */
+enum {
+  Q2_ERR_NONFINITE = 1u,  /* "input must be finite"              quantizers.py:118-119 */
+  Q2_ERR_SCALE448  = 2u,  /* corrected scale exceeds 448         ms_eden.py:144-149, posthoc.py:115-122 */
+  Q2_ERR_NAN_SCALE = 4u,  /* NaN reached encode_fp8_rtn          formats.py:167-168 */
+  Q2_ERR_E8M3_OVF  = 8u   /* round_e8m3_rtn overflow             formats.py:223-224 */
+};
+
+typedef struct {
+  uint8_t* codes;
+  uint8_t* sf;
+  float*   scale32;
+  int64_t  R, K;
+} q2_nvfp4;
+
+/* Bytes of the swizzled scale-factor buffer for a [R, K] tensor. */
+size_t q2_sf_bytes(int64_t R, int64_t K);
+
+/* Library build info (arch string); used by the loader's self-check. */
+const char* q2_version(void);
+
+/* Per-tensor |x| max as float bits (x is bf16/fp32, exact), OR-ing
+ * Q2_ERR_NONFINITE into err.  amax must be zeroed by the caller (or use
+ * q2_quant_fwd which does it).                                                  */
+int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
+            uint32_t* amax_bits, uint32_t* err, void* stream);
+
+/* Forward quantizer family (one pass over x after the amax pass).
+ *  quantize_rtn_46(x, caps, scale_cap)   quantizers.py:206-234
+ *      ncaps = 2, caps = {c0, c1}, scale_div = c0*scale_cap (host float64)
+ *  quantize_rtn(x, s)                    quantizers.py:164-181
+ *      ncaps = 1, caps = {s}, scale_div = s*256
+ *  scale32 = (float)(absmax / scale_div); per group s8 = E4M3_RTN(gmax /
+ *  (scale32*c)); codes by ties-to-even RTN; with two caps the branch with the
+ *  strictly lower sequential float64 squared error wins (ties keep caps[0]).
+ *  ws: q2_quant_fwd_ws_bytes() bytes of device scratch.                        */
+size_t q2_quant_fwd_ws_bytes(void);
+int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
+                 int ncaps, double cap0, double cap1, double scale_div,
+                 const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);
+
+/* MS-EDEN backward quantizer (randomized 128-Hadamard + clipping RTN cap 256 +
+ * per-chunk EDEN factor + stochastic E4M3 scale rounding).
+ *  ms_eden_quantize(x, seeds, s, tensor_id, rotation_id, pow2_scale)
+ *      ms_eden.py:116-153     mode Q2_MSED_EXACT / Q2_MSED_POW2
+ *  pass2(pass1(x, seed_rht, s, tensor_id, rotation_id), seed_sr, tensor_id)
+ *      posthoc.py:74-125      mode Q2_MSED_POSTHOC (single read of x)
+ * The quantized logical tensor is [R, K], grouped/rotated along K:
+ *  Q2_SRC_ROWS     x is bf16/fp32 [R, K] with row stride ld (elements).
+ *  Q2_SRC_COLS     x is bf16/fp32 [K, R] with row stride ld: quantizes x^T
+ *                  (E^T for the wgrad GEMM) without materialising it.
+ *  Q2_SRC_TAPE_COLS x is an NVFP4 tensor `tape` of logical shape [K, R]
+ *                  (qW or qX saved by the forward); quantizes dequant(tape)^T
+ *                  (W^T / X^T of linear_graph.py:293-294, 304, 322-323).
+ * sign_mask: 128-bit sign vector (4 x u32, bit i = sign i negative) for the
+ * rotation stream (rht.py:99-106); sr_stream = derive_stream(0x5343414C,
+ * tensor_id) (ms_eden.py:150).  inv_sqrt_chunk is 128**-0.5 as the host
+ * computes it.  ws: q2_msed_ws_bytes(R, K) bytes of device scratch.           */
+enum { Q2_SRC_ROWS = 0, Q2_SRC_COLS = 1, Q2_SRC_TAPE_COLS = 2 };
+enum { Q2_MSED_EXACT = 0, Q2_MSED_POW2 = 1, Q2_MSED_POSTHOC = 2 };
+size_t q2_msed_ws_bytes(int64_t R, int64_t K);
+int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind,
+                  int64_t R, int64_t K, int64_t ld, const uint32_t sign_mask[4],
+                  double s, double inv_sqrt_chunk, uint64_t seed_sr, uint64_t sr_stream,
+                  int mode, const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);
+
+/* Post-hoc pass 1 alone (posthoc.py:74-95): codes written to out->codes,
+ * E8M3 pseudo-scales as bf16 [R, K/16], EDEN factors as float64 [R, K/128],
+ * rotated absmax and pseudo-scale max as float bits in red[0], red[1].
+ * pass 2 alone (posthoc.py:98-125) reads pseudo/corr/red and writes out->sf,
+ * out->scale32.                                                              */
+int q2_posthoc_pass1(const void* x, int dtype, const q2_nvfp4* tape, int src_kind,
+                     int64_t R, int64_t K, int64_t ld, const uint32_t sign_mask[4],
+                     double s, double inv_sqrt_chunk, uint8_t* codes,
+                     uint16_t* pseudo_bf16, double* corr, uint32_t* red,
+                     uint32_t* err, void* stream);
+int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr, const uint32_t* red,
+                     int64_t R, int64_t K, uint64_t seed_sr, uint64_t sr_stream,
+                     const q2_nvfp4* out, uint32_t* err, void* stream);
+
+/* NVFP4 "TN" GEMM on tcgen05 block-scaled MMAs (kind::mxf4nvf4, UE4M3 scales
+ * per 16, FP32 accumulation in TMEM):  D[M, N] = alpha * A[M,K] . B[N,K]^T
+ * with alpha = *a->scale32 * *b->scale32 (+ beta*D if accumulate).
+ * Replaces gemm_emulated (linear_graph.py:190-205) for the fprop, dgrad and
+ * wgrad GEMMs.  d_dtype Q2_BF16 or Q2_F32; d row stride ldd (elements).
+ * K % 64 == 0; K/2 % 16 == 0.                                                */
+int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_dtype, int64_t ldd,
+               int accumulate, void* stream);
+
+/* Helpers used by the host mirror: dequantize (quantizers.py:315-323) into
+ * float64 [R, K]; unpack codes/scales into the reference's unpacked layout
+ * (fp4 uint8 [R, K], scales8 uint8 [R, K/16]).                               */
+int q2_dequant(const q2_nvfp4* t, double* out, void* stream);
+int q2_unpack(const q2_nvfp4* t, uint8_t* fp4, uint8_t* scales8, void* stream);
+int q2_pack(const uint8_t* fp4, const uint8_t* scales8, const q2_nvfp4* t, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUARTET2_H_ */

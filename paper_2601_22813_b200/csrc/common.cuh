@@ -1,0 +1,136 @@
+// Shared device helpers for the Quartet II kernels (sm_100a).
+//
+// Everything here reproduces a float64 decision of the reference emulator
+// bit-for-bit; the reference line each helper restates is cited.  Literal
+// float64 arithmetic uses __d*_rn intrinsics so nvcc never contracts it into
+// an FMA (the reference is numpy/numba without fastmath).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/quartet2.h"
+
+namespace q2 {
+
+constexpr int GROUP = 16;
+constexpr int CHUNK = 128;
+
+// ---------------------------------------------------------------- layout ----
+// Byte offset of scale (r, j) in the tcgen05 block-scale atom layout
+// (128x4 atoms of 512 B, K-fastest).  See include/quartet2.h.
+__host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t j, int64_t kb64) {
+  return (((r >> 7) * kb64 + (j >> 2)) << 9) + ((r & 31) << 4) + (((r >> 5) & 3) << 2) + (j & 3);
+}
+__host__ __device__ __forceinline__ int64_t kblocks64(int64_t K) { return (K + 63) / 64; }
+
+// ------------------------------------------------------------------ E2M1 ----
+// magnitude code -> value (formats.py:43-46); code 8 is +0.
+__device__ __forceinline__ double fp4_val(uint32_t code) {
+  const double mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  double v = mag[code & 7];
+  return (code & 8) ? -v : v;
+}
+__device__ __forceinline__ float fp4_valf(uint32_t code) {
+  const float mag[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+  float v = mag[code & 7];
+  return (code & 8) ? -v : v;
+}
+
+// ------------------------------------------------------------------ E4M3 ----
+// Decode a non-negative E4M3 code (0..126) (formats.py:53-66).
+__host__ __device__ __forceinline__ double e4m3_val(uint32_t code) {
+  uint32_t e = (code >> 3) & 0xF, m = code & 7;
+  if (e == 0) return (double)m * 0x1p-9;
+  return (double)(8 + m) * ldexp(1.0, (int)e - 10);
+}
+
+// Nearest E4M3 code, ties to the even code, saturating at 448 (code 126).
+// Restates formats._nearest_even_index over the 126 exact midpoints
+// (formats.py:85-94, 160-171).  x >= 0, not NaN.
+__device__ __forceinline__ uint32_t e4m3_rtn(double x) {
+  if (!(x < 432.0)) return 126u;                       // 432 is the top midpoint (tie -> 126, even)
+  if (x < 0x1p-6) return (uint32_t)rint(x * 512.0);    // subnormal spacing 2^-9, rint = RNE
+  int e = ilogb(x);                                    // x in [2^e, 2^(e+1)), e in [-6, 8]
+  double f = __dsub_rn(ldexp(x, -e), 1.0);             // exact
+  uint32_t q = (uint32_t)rint(f * 8.0);                // RNE on the mantissa; q == 8 carries
+  uint32_t code = ((uint32_t)(e + 7) << 3) + q;
+  return code > 126u ? 126u : code;
+}
+
+// Stochastic E4M3 rounding; RTN below 2^-6 (formats.py:174-201).  x <= 448(1+1e-9).
+__device__ __forceinline__ uint32_t e4m3_sr(double x, double u) {
+  if (x < 0x1p-6) return e4m3_rtn(x);
+  x = fmin(x, 448.0);
+  int e = ilogb(x);
+  double f = __dsub_rn(ldexp(x, -e), 1.0);
+  uint32_t lo = ((uint32_t)(e + 7) << 3) + (uint32_t)floor(f * 8.0);
+  if (lo > 125u) lo = 125u;
+  double a = e4m3_val(lo), b = e4m3_val(lo + 1);
+  double p = __ddiv_rn(__dsub_rn(x, a), __dsub_rn(b, a));
+  return lo + (u < p ? 1u : 0u);
+}
+
+// Round to the E8M3 grid (4 significant bits, bf16 exponent range)
+// (formats.py:204-229).  Sets *ovf on overflow.
+__device__ __forceinline__ double e8m3_rtn(double x, bool* ovf) {
+  if (x < 0x1p-126) return (x <= 0x1p-127) ? 0.0 : 0x1p-126;
+  int e;
+  double m = frexp(x, &e);                // m in [0.5, 1)
+  double q = rint(16.0 * m);
+  if (q >= 16.0) { q = 8.0; e += 1; }
+  if (e - 1 > 127) *ovf = true;
+  return ldexp(q / 16.0, e);
+}
+
+// ------------------------------------------------------------ element RTN ---
+// Literal _nb_rtn (_kernels.py:101-127) for a float64 value: q = v/d (d<=0 ->
+// q = +0), a2 = min(2|q|, 12), banker's rounding on the doubled grid.
+__device__ __forceinline__ uint32_t rtn_code_literal(double v, double d) {
+  double q = d > 0.0 ? __ddiv_rn(v, d) : 0.0;
+  double a2 = fmin(fabs(q) * 2.0, 12.0);
+  double r = a2 <= 4.0 ? rint(a2) : (a2 <= 8.0 ? 2.0 * rint(a2 * 0.5) : 4.0 * rint(a2 * 0.25));
+  uint32_t ri = (uint32_t)r;               // 0,1,2,3,4,6,8,12
+  uint32_t mag = ri <= 4 ? ri : (ri == 6 ? 5u : (ri == 8 ? 6u : 7u));
+  return mag | (signbit(q) ? 8u : 0u);
+}
+
+// Exact-threshold RTN for a value whose float64 quotient v/d decides exactly
+// like the rational (v an fp32/bf16, d = E4M3 * fp32): count the ties-to-even
+// thresholds t*d with t in {.25 .75 1.25 1.75 2.5 3.5 5} (down, up, down, ...)
+// crossed by |v|.  T[] holds t*d (exact in float64).
+__device__ __forceinline__ uint32_t rtn_mag_thresholds(double a, const double* T) {
+  uint32_t c = 0;
+  c += a > T[0]; c += a >= T[1]; c += a > T[2]; c += a >= T[3];
+  c += a > T[4]; c += a >= T[5]; c += a > T[6];
+  return c;
+}
+
+// ------------------------------------------------------------------- PRNG ---
+// splitmix64 finalizer chain (rht.py:36-39, 57-68, 89-96).
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// The (seed, stream) prefix of _bits, shared by every index of one stream.
+__host__ __device__ __forceinline__ uint64_t prng_head(uint64_t seed, uint64_t stream) {
+  return mix64(mix64(seed + GOLDEN) ^ (stream + GOLDEN));
+}
+__device__ __forceinline__ double prng_uniform(uint64_t head, uint64_t index) {
+  uint64_t z = mix64(head ^ (index + GOLDEN));
+  return (double)(z >> 11) * 0x1p-53;
+}
+
+// ------------------------------------------------------------------ loads ---
+__device__ __forceinline__ float bf16_to_f32(uint32_t bits16) { return __uint_as_float(bits16 << 16); }
+
+__device__ __forceinline__ void atomic_or_err(uint32_t* err, uint32_t bits) {
+  if (err) atomicOr(err, bits);
+}
+
+}  // namespace q2
+
+#define Q2_CHECK_LAUNCH()                                 \
+  do {                                                    \
+    if (cudaGetLastError() != cudaSuccess) return Q2_ECUDA; \
+  } while (0)

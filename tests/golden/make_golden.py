@@ -1,0 +1,66 @@
+"""Generate golden vectors by running the REFERENCE (nvfp4emu) in this container.
+
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py
+
+Writes tests/golden/golden.npz.  The reference lives at /root/reference and
+does not travel to the GPU box, so its outputs are frozen here; the oracle is
+pinned against them by tests/test_oracle_pin.py.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import nvfp4emu as R  # noqa: E402
+from nvfp4emu import linear_graph as LG, ms_eden as ME, posthoc as PH, rht as RH  # noqa: E402
+
+from tests.families import FAMILIES, make  # noqa: E402
+
+
+def pack(prefix, t, out):
+    out[prefix + "fp4"] = t.fp4
+    out[prefix + "s8"] = t.scales8
+    out[prefix + "s32"] = np.float32(t.scale32)
+
+
+def main():
+    out = {}
+    seeds = RH.SeedPair(123, 456)
+    for fam in FAMILIES:
+        for bf16 in (True, False):
+            x = make(fam, (64, 256), seed=31, bf16=bf16)
+            key = f"{fam}_{'bf16' if bf16 else 'f32'}_"
+            out[key + "x"] = x
+            pack(key + "q46_", R.quantize_rtn_46(x), out)
+            pack(key + "rtn_", R.quantize_rtn(x), out)
+            pack(key + "msed_", ME.ms_eden_quantize(x, seeds, tensor_id=77, rotation_id=99), out)
+            pack(key + "pow2_", ME.ms_eden_quantize(x, seeds, tensor_id=77, rotation_id=99, pow2_scale=True), out)
+            er, red = PH.pass1(x, seeds.rht, tensor_id=77, rotation_id=99)
+            pack(key + "posthoc_", PH.pass2(er, red, seeds.sr, tensor_id=77), out)
+    # end-to-end digest case of SURVEY.md §8(c)
+    rng = np.random.default_rng(2026)
+    X = rng.standard_normal((128, 256)).astype(np.float32)
+    W = (rng.standard_normal((256, 256)) / 16).astype(np.float32)
+    E = (1e-2 * rng.standard_normal((128, 256))).astype(np.float32)
+    y, tape = LG.forward(X, W, LG.baseline_config("quartet2"))
+    g = LG.backward(tape, E, RH.SeedPair(7, 9))
+    out.update(e2e_X=X, e2e_W=W, e2e_E=E, e2e_Y=y, e2e_dX=g.dX, e2e_dW=g.dW)
+    pack("e2e_qX_", tape.qX, out)
+    pack("e2e_qW_", tape.qW, out)
+    # PRNG known answers
+    out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
+    out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))
+    out["kat_signs_pair_dx"] = RH._sign_vector(0, RH.derive_stream(1), 128)
+    out["kat_streams"] = np.array([RH.derive_stream(1), RH.derive_stream(2), RH.derive_stream("mse-data", 0)],
+                                  dtype=np.uint64)
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
+    print("wrote", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()

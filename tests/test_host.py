@@ -1,0 +1,72 @@
+"""CPU tests: the C ABI loads and exports every declared symbol; host-side
+integer ports (stream ids, sign masks) agree with the oracle; API validation
+that needs no device."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import nvfp4_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_header_symbols():
+    from paper_2601_22813_b200 import _lib
+    header = open(os.path.join(ROOT, "include", "quartet2.h")).read()
+    declared = set(re.findall(r"\b(q2_[a-z0-9_]+)\s*\(", header))
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    lib = _lib.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.q2_version().startswith(b"quartet2-b200")
+
+
+def test_sf_bytes():
+    from paper_2601_22813_b200 import _lib
+    L = _lib.lib()
+    assert L.q2_sf_bytes(128, 64) == 512
+    assert L.q2_sf_bytes(129, 64) == 1024
+    assert L.q2_sf_bytes(128, 256) == 2048
+    assert L.q2_sf_bytes(256, 80) == 2 * 2 * 512
+
+
+def test_host_streams_match_oracle():
+    import paper_2601_22813_b200 as q2
+    for parts in [(1,), (2,), ("mse-data", 0), (q2.PAIR_DX, 0), (q2.PAIR_DW, 1), (2**64 - 1, 5)]:
+        assert q2.derive_stream(*parts) == O.derive_stream(*parts)
+    for seed, rot in [(0, q2.PAIR_DX), (7, q2.PAIR_DW), (2**63 + 5, 3)]:
+        w = q2.sign_mask(seed, rot)
+        assert sum(v << (32 * i) for i, v in enumerate(w)) == O.sign_mask(seed, rot)
+    for idx in (0, 1, 12345, 2**40):
+        assert q2.prng_uniform(9, 77, idx) == float(O.prng_uniform(9, 77, idx))
+
+
+def test_sf_layout_formula():
+    """SF byte offsets match the CuTe blockscaled atom ((32,4),(16,4)):((16,4),(0,1))."""
+    def off(r, j, K):
+        kb = (K + 63) // 64
+        return ((r // 128) * kb + j // 4) * 512 + (r % 32) * 16 + ((r % 128) // 32) * 4 + j % 4
+    K, R = 256, 256
+    seen = {off(r, j, K) for r in range(R) for j in range(K // 16)}
+    assert len(seen) == R * K // 16 and max(seen) < R * K // 16
+
+
+def test_layer_config_validation():
+    import paper_2601_22813_b200 as q2
+    with pytest.raises(ValueError):
+        q2.LayerConfig(forward_scheme="rtn_16x16")
+    with pytest.raises(ValueError):
+        q2.LayerConfig(reuse_forward_weights=True)
+    with pytest.raises(ValueError):
+        q2.baseline_config("nvidia")
+    assert q2.baseline_config("quartet2") == q2.LayerConfig()
+
+
+def test_constants_match_reference_arithmetic():
+    import paper_2601_22813_b200 as q2
+    assert (6.0 * q2.GUARDED_SCALE_CAP).hex() == "0x1.3c3c3c3c3c3c4p+11"
+    from paper_2601_22813_b200.rht import INV_SQRT_CHUNK
+    assert INV_SQRT_CHUNK.hex() == "0x1.6a09e667f3bcdp-4"
