@@ -9,7 +9,12 @@ mkdir -p build
 objs=""
 for f in $SRC; do
   o=build/$(basename "${f%.cu}").o
-  if [ ! -f "$o" ] || [ "$f" -nt "$o" ] || [ paper_2601_22813_b200/csrc/common.cuh -nt "$o" ] || [ include/quartet2.h -nt "$o" ]; then
+  stale=0
+  [ -f "$o" ] || stale=1
+  for dep in "$f" paper_2601_22813_b200/csrc/*.cuh include/quartet2.h; do
+    [ "$dep" -nt "$o" ] && stale=1
+  done
+  if [ "$stale" = 1 ]; then
     "$NVCC" -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC \
       -Xptxas -v -c "$f" -o "$o" 2> "build/$(basename "${f%.cu}").ptxas.log" || { cat "build/$(basename "${f%.cu}").ptxas.log"; exit 1; }
   fi

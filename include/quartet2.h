@@ -77,8 +77,10 @@ int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
  *  scale32 = (float)(absmax / scale_div); per group s8 = E4M3_RTN(gmax /
  *  (scale32*c)); codes by ties-to-even RTN; with two caps the branch with the
  *  strictly lower sequential float64 squared error wins (ties keep caps[0]).
- *  ws: q2_quant_fwd_ws_bytes() bytes of device scratch.                        */
-size_t q2_quant_fwd_ws_bytes(void);
+ *  ws: q2_quant_fwd_ws_bytes(R, K) bytes of device scratch (tensor absmax and
+ *  the list of groups the certified fp32 fast path hands to the exact
+ *  float64 fix-up kernel).                                                     */
+size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K);
 int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
                  int ncaps, double cap0, double cap1, double scale_div,
                  const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);

@@ -46,7 +46,7 @@ _SIGS = {
     "q2_sf_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "q2_version": (ctypes.c_char_p, []),
     "q2_amax": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P]),
-    "q2_quant_fwd_ws_bytes": (ctypes.c_size_t, []),
+    "q2_quant_fwd_ws_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "q2_quant_fwd": (_I, [_P, _I, _I64, _I64, _I64, _I, _D, _D, _D, _TP, _P, _P, _P]),
     "q2_msed_ws_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "q2_msed_quant": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _U64, _U64, _I, _TP, _P, _P, _P]),

@@ -12,6 +12,7 @@
 // The rotation is the literal float64 butterfly network of _nb_fwht
 // (_kernels.py:175-187): every output of every stage is one IEEE add/sub of
 // two stage inputs, so the result does not depend on which lane computes it.
+#include <cuda_fp16.h>
 #include "common.cuh"
 
 namespace q2 {
@@ -294,6 +295,158 @@ __global__ void __launch_bounds__(MSED_THREADS) msed_kernel(MsedArgs a) {
   }
 }
 
+// --------------------------------------------------------- literal fix-ups --
+// Warp-level gather of one (row, chunk) unit, signs applied: lane l holds
+// elements 4l..4l+3 as float64 (tape: FP4*E4M3*scale32, exact).
+template <int SRC>
+__device__ __forceinline__ void load_chunk_lit(const MsedArgs& a, int64_t r, int64_t c, int lane, double (&y)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = 4 * lane + i;
+    const int64_t k = c * CHUNK + e;
+    double v;
+    if (SRC == Q2_SRC_ROWS || SRC == Q2_SRC_COLS) {
+      const int64_t off = SRC == Q2_SRC_ROWS ? r * a.ld + k : k * a.ld + r;
+      v = a.dtype == Q2_BF16 ? (double)bf16_to_f32(static_cast<const uint16_t*>(a.x)[off])
+                             : (double)static_cast<const float*>(a.x)[off];
+    } else {
+      const uint32_t byte = a.tape_codes[k * (a.R / 2) + r / 2];
+      const uint32_t code = (r & 1) ? byte >> 4 : byte & 0xF;
+      const uint32_t s8 = a.tape_sf[sf_offset(k, r / 16, kblocks64(a.R))];
+      v = __dmul_rn(__dmul_rn(fp4_val(code), e4m3_val(s8)), (double)*a.tape_scale32);
+    }
+    y[i] = ((a.sign[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+  }
+}
+
+// Literal posthoc pass 1 of one chunk (posthoc.py:74-95): returns S; writes
+// codes and pseudo-scales when `write`; reduces the pseudo max into *pmx.
+template <int SRC>
+__device__ __forceinline__ double posthoc1_chunk_lit(const MsedArgs& a, int64_t r, int64_t c, int lane, double* pn,
+                                                     double* pd, bool write, double* pmx, bool* ovf) {
+  double y[4];
+  load_chunk_lit<SRC>(a, r, c, lane, y);
+  fwht_f64(y, lane);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] = __dmul_rn(y[i], a.inv_sqrt);
+  const double lmax = fmax(fmax(fabs(y[0]), fabs(y[1])), fmax(fabs(y[2]), fabs(y[3])));
+  const double gmax = group_max4(lmax);
+  const double d = e8m3_rtn(__ddiv_rn(gmax, a.s), ovf);
+  *pmx = fmax(*pmx, d);
+  uint32_t codes = 0;
+  double dq[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t cd = rtn_code_literal(y[i], d);
+    codes |= cd << (4 * i);
+    dq[i] = __dmul_rn(fp4_val(cd), d);
+  }
+  if (write) {
+    *reinterpret_cast<uint16_t*>(a.codes + r * (a.K / 2) + c * 64 + 2 * lane) = (uint16_t)codes;
+    if ((lane & 3) == 0) a.pseudo[r * (a.K / GROUP) + c * 8 + (lane >> 2)] = (uint16_t)(__float_as_uint((float)d) >> 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    pn[4 * lane + i] = __dmul_rn(y[i], y[i]);
+    pd[4 * lane + i] = __dmul_rn(y[i], dq[i]);
+  }
+  __syncwarp();
+  const double num = numpy_sum128(pn, lane);
+  const double den = numpy_sum128(pd, lane);
+  __syncwarp();
+  const bool ok = (fabs(den) >= __dmul_rn(1e-30, num)) && (num > 0.0);
+  return ok ? __ddiv_rn(num, den) : 1.0;
+}
+
+// Fix-up of pass-1 chunks the fast path could not certify.
+template <int SRC>
+__global__ void __launch_bounds__(128) posthoc_fix1_kernel(MsedArgs a, float* dS, const uint32_t* listA_n,
+                                                           const uint32_t* listA) {
+  __shared__ double scratch[4][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = *listA_n, cpr = (uint32_t)(a.K / CHUNK);
+  double pmx = 0.0;
+  bool ovf = false;
+  for (uint32_t i = blockIdx.x * 4 + warp; i < n; i += gridDim.x * 4) {
+    const uint32_t id = listA[i];
+    const int64_t r = id / cpr, c = id % cpr;
+    const double S = posthoc1_chunk_lit<SRC>(a, r, c, lane, scratch[warp], scratch[warp] + 128, true, &pmx, &ovf);
+    if (lane == 0) { a.corr[id] = S; dS[id] = 0.f; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pmx = fmax(pmx, __shfl_xor_sync(0xFFFFFFFFu, pmx, o));
+  if (lane == 0 && pmx > 0.0) atomicMax(&a.red[1], (unsigned long long)__double_as_longlong(pmx));
+  if (ovf) atomic_or_err(a.err, Q2_ERR_E8M3_OVF);
+}
+
+__device__ __forceinline__ float posthoc_scale32(double pmax) {
+  if (!(pmax > 0.0)) return 0.f;
+  int e; const double m = frexp(pmax / 256.0, &e);
+  return (float)ldexp(1.0, (m == 0.5) ? e - 1 : e);         // ms_eden.py:86-91
+}
+
+// Certified pass 2 (posthoc.py:98-125): one thread per group; the SR decision
+// must agree at both ends of corr * (1 -+ dS), else the group is re-done by
+// posthoc_fix2_kernel with the exact float64 factor.
+__global__ void posthoc2_cert_kernel(const uint16_t* __restrict__ pseudo, const double* __restrict__ corr,
+                                     const float* __restrict__ dS, const unsigned long long* __restrict__ red,
+                                     int64_t R, int64_t K, uint64_t sr_head, uint8_t* __restrict__ sf,
+                                     float* __restrict__ scale32_out, uint32_t* __restrict__ listB_n,
+                                     uint32_t* __restrict__ listB, uint32_t* __restrict__ err) {
+  const int64_t gpr = K / GROUP, total = R * gpr;
+  const double pmax = ulong_as_double(red[1]);
+  const float scale32 = posthoc_scale32(pmax);
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g == 0) *scale32_out = scale32;
+  if (g >= total) return;
+  const int64_t r = g / gpr, j = g - r * gpr;
+  uint8_t* out = sf + sf_offset(r, j, kblocks64(K));
+  if (pmax == 0.0) { *out = 0; return; }
+  const double ps = (double)__uint_as_float((uint32_t)pseudo[g] << 16);
+  const double shifted = __ddiv_rn(ps, (double)scale32);
+  const int64_t ch = r * (K / CHUNK) + j / 8;
+  const double S = corr[ch];
+  const double u = prng_uniform(sr_head, (uint64_t)g);
+  const float d = dS[ch];
+  if (d == 0.f) {
+    const double corrected = __dmul_rn(S, shifted);
+    if (corrected > 448.0) atomic_or_err(err, Q2_ERR_SCALE448);
+    *out = (uint8_t)e4m3_sr(fmin(corrected, 448.0), u);
+    return;
+  }
+  const double cm = __dmul_rn(S, shifted);
+  const double lo = cm * (1.0 - (double)d), hi = cm * (1.0 + (double)d);
+  const uint32_t clo = e4m3_sr(fmin(lo, 448.0), u), chi = e4m3_sr(fmin(hi, 448.0), u);
+  if (clo == chi && hi <= 448.0 && d < 1e-3f) { *out = (uint8_t)clo; return; }
+  listB[atomicAdd(listB_n, 1u)] = (uint32_t)g;
+}
+
+// Exact re-do of pass-2 groups (exact float64 EDEN factor of their chunk).
+template <int SRC>
+__global__ void __launch_bounds__(128) posthoc_fix2_kernel(MsedArgs a, const uint32_t* listB_n, const uint32_t* listB,
+                                                           uint64_t sr_head) {
+  __shared__ double scratch[4][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = *listB_n;
+  const int64_t gpr = a.K / GROUP;
+  const double pmax = ulong_as_double(a.red[1]);
+  const float scale32 = posthoc_scale32(pmax);
+  for (uint32_t i = blockIdx.x * 4 + warp; i < n; i += gridDim.x * 4) {
+    const uint32_t g = listB[i];
+    const int64_t r = g / gpr, j = g - r * gpr;
+    double pm = 0.0;
+    bool ovf = false;
+    const double S = posthoc1_chunk_lit<SRC>(a, r, j / 8, lane, scratch[warp], scratch[warp] + 128, false, &pm, &ovf);
+    if (lane == 0) {
+      const double ps = (double)__uint_as_float((uint32_t)a.pseudo[g] << 16);
+      const double corrected = __dmul_rn(S, __ddiv_rn(ps, (double)scale32));
+      if (corrected > 448.0) atomic_or_err(a.err, Q2_ERR_SCALE448);
+      a.sf[sf_offset(r, j, kblocks64(a.K))] =
+          (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g));
+    }
+  }
+}
+
 // posthoc pass 2: scales only (posthoc.py:98-125).  One thread per group.
 __global__ void posthoc2_kernel(const uint16_t* __restrict__ pseudo, const double* __restrict__ corr,
                                 const unsigned long long* __restrict__ red, int64_t R, int64_t K,
@@ -318,6 +471,10 @@ __global__ void posthoc2_kernel(const uint16_t* __restrict__ pseudo, const doubl
   if (corrected > 448.0) atomic_or_err(err, Q2_ERR_SCALE448);
   *out = (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g));
 }
+
+}  // namespace q2
+#include "msed_fast.cuh"
+namespace q2 {
 
 constexpr size_t MSED_SMEM = TILE_ROWS * TILE_LD * sizeof(float) + 8 * 256 * sizeof(double);
 
@@ -367,14 +524,52 @@ static int fill_args(MsedArgs& a, const void* x, int dtype, const q2_nvfp4* tape
   return Q2_OK;
 }
 
+template <int SRC, int DT>
+static int launch_fast1(const MsedArgs& a, const FastArgs& f, cudaStream_t st) {
+  const int smem = F_ROWS * (DT == Q2_BF16 ? 256 : 512) + 256;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(msed_fast1_kernel<SRC, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return Q2_ECUDA;
+    attr = true;
+  }
+  dim3 grid((unsigned)((a.R + F_ROWS - 1) / F_ROWS), (unsigned)(a.K / CHUNK));
+  msed_fast1_kernel<SRC, DT><<<grid, F_THREADS, smem, st>>>(a, f);
+  Q2_CHECK_LAUNCH();
+  return Q2_OK;
+}
+
+// Single-read post-hoc MS-EDEN with certified fast paths and exact fix-ups.
+template <int SRC>
+static int posthoc_fast(MsedArgs a, FastArgs f, uint32_t* listB_n, uint32_t* listB, uint64_t sr_head,
+                        cudaStream_t st) {
+  int rc = (SRC == Q2_SRC_TAPE_COLS || a.dtype == Q2_BF16) ? launch_fast1<SRC, Q2_BF16>(a, f, st)
+                                                            : launch_fast1<SRC, Q2_F32>(a, f, st);
+  if (rc) return rc;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  posthoc_fix1_kernel<SRC><<<2 * nsm, 128, 0, st>>>(a, f.dS, f.listA_n, f.listA);
+  Q2_CHECK_LAUNCH();
+  const int64_t groups = a.R * (a.K / GROUP);
+  posthoc2_cert_kernel<<<(unsigned)std::max<int64_t>(1, (groups + 255) / 256), 256, 0, st>>>(
+      a.pseudo, a.corr, f.dS, a.red, a.R, a.K, sr_head, a.sf, a.scale32, listB_n, listB, a.err);
+  Q2_CHECK_LAUNCH();
+  posthoc_fix2_kernel<SRC><<<2 * nsm, 128, 0, st>>>(a, listB_n, listB, sr_head);
+  Q2_CHECK_LAUNCH();
+  return Q2_OK;
+}
+
 }  // namespace q2
 
 using namespace q2;
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// ws: red | pseudo bf16 [R,K/16] | corr f64 [R,K/128] | dS f32 [R,K/128] | listA | listB
 extern "C" size_t q2_msed_ws_bytes(int64_t R, int64_t K) {
-  return 256 + align256((size_t)R * (K / 16) * 2) + align256((size_t)R * (K / 128) * 8);
+  const size_t g = (size_t)R * (K / 16), ch = (size_t)R * (K / 128);
+  return 256 + align256(g * 2) + align256(ch * 8) + align256(ch * 4) + align256(ch * 4) + align256(g * 4);
 }
 
 extern "C" int q2_posthoc_pass1(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R,
@@ -419,10 +614,27 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   uint16_t* pseudo = reinterpret_cast<uint16_t*>(w + 256);
   double* corr = reinterpret_cast<double*>(w + 256 + align256((size_t)R * (K / 16) * 2));
   if (mode == Q2_MSED_POSTHOC) {
-    rc = q2_posthoc_pass1(x, dtype, tape, src_kind, R, K, ld, sign_mask, s, inv_sqrt_chunk, out->codes,
-                          pseudo, corr, red, err, stream);
-    if (rc) return rc;
-    return q2_posthoc_pass2(pseudo, corr, red, R, K, seed_sr, sr_stream, out, err, stream);
+    const size_t g = (size_t)R * (K / 16), ch = (size_t)R * (K / 128);
+    char* p = w + 256 + align256(g * 2) + align256(ch * 8);
+    FastArgs f;
+    f.dS = reinterpret_cast<float*>(p);
+    p += align256(ch * 4);
+    f.listA = reinterpret_cast<uint32_t*>(p);
+    p += align256(ch * 4);
+    uint32_t* listB = reinterpret_cast<uint32_t*>(p);
+    uint32_t* cnt = red + 4;                 // red[0..3]: two f64 maxima; [4] listA_n, [5] listB_n
+    f.listA_n = cnt;
+    if (cudaMemsetAsync(red, 0, 32, st) != cudaSuccess) return Q2_ECUDA;
+    if (R == 0) return Q2_OK;
+    a.red = reinterpret_cast<unsigned long long*>(red); a.err = err;
+    a.codes = out->codes; a.sf = out->sf; a.scale32 = out->scale32;
+    a.pseudo = pseudo; a.corr = corr;
+    const uint64_t head = prng_head(seed_sr, sr_stream);
+    switch (src_kind) {
+      case Q2_SRC_ROWS: return posthoc_fast<Q2_SRC_ROWS>(a, f, cnt + 1, listB, head, st);
+      case Q2_SRC_COLS: return posthoc_fast<Q2_SRC_COLS>(a, f, cnt + 1, listB, head, st);
+      default: return posthoc_fast<Q2_SRC_TAPE_COLS>(a, f, cnt + 1, listB, head, st);
+    }
   }
   if (mode != Q2_MSED_EXACT && mode != Q2_MSED_POW2) return Q2_EINVAL;
   a.red = reinterpret_cast<unsigned long long*>(red); a.err = err;

@@ -36,59 +36,79 @@ __device__ __forceinline__ bool nonfinite(float f) {
   return (__float_as_uint(f) & 0x7F800000u) == 0x7F800000u;
 }
 
-// |x| max over a [R, K] view (K % 8 == 0), as float bits; flags non-finite.
-__global__ void amax_kernel(const void* __restrict__ x, int dtype, int64_t R, int64_t K, int64_t ld,
-                            uint32_t* __restrict__ amax_bits, uint32_t* __restrict__ err) {
-  const int64_t per_row = K / 8, total = R * per_row;
-  float m = 0.f;
-  bool bad = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i / per_row, c = (i - r * per_row) * 8;
-    float v[8];
-    load_vec8(x, dtype, r * ld + c, v);
+// |x| max as float bits; flags non-finite.  Contiguous views stream 32-byte
+// vectors (no index arithmetic); strided views walk rows.
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&w)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void absmax_words(const uint32_t (&w)[8], int dtype, uint32_t& m, bool& bad) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      bad |= nonfinite(v[k]);
-      m = fmaxf(m, fabsf(v[k]));
+  for (int i = 0; i < 8; ++i) {
+    if (dtype == Q2_BF16) {
+      const uint32_t a = w[i] & 0x7FFF7FFFu;
+      bad |= ((a & 0x7F80u) == 0x7F80u) | ((a & 0x7F800000u) == 0x7F800000u);
+      asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(a));
+    } else {
+      const uint32_t a = w[i] & 0x7FFFFFFFu;
+      bad |= a >= 0x7F800000u;
+      m = max(m, a);
     }
   }
+}
+__global__ void __launch_bounds__(256) amax_kernel(const void* __restrict__ x, int dtype, int64_t R, int64_t K,
+                                                   int64_t ld, uint32_t* __restrict__ amax_bits,
+                                                   uint32_t* __restrict__ err) {
+  const int esz = dtype == Q2_BF16 ? 2 : 4;
+  uint32_t m = 0;
+  bool bad = false;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  const char* base = static_cast<const char*>(x);
+  if (ld == K) {
+    const int64_t nvec = R * K * esz / 32;
+    int64_t i = tid;
+    for (; i + 3 * nth < nvec; i += 4 * nth) {
+      uint32_t w0[8], w1[8], w2[8], w3[8];
+      ld256(base + 32 * i, w0); ld256(base + 32 * (i + nth), w1);
+      ld256(base + 32 * (i + 2 * nth), w2); ld256(base + 32 * (i + 3 * nth), w3);
+      absmax_words(w0, dtype, m, bad); absmax_words(w1, dtype, m, bad);
+      absmax_words(w2, dtype, m, bad); absmax_words(w3, dtype, m, bad);
+    }
+    for (; i < nvec; i += nth) {
+      uint32_t w0[8];
+      ld256(base + 32 * i, w0);
+      absmax_words(w0, dtype, m, bad);
+    }
+  } else {
+    const int64_t per_row = K * esz / 32;
+    for (int64_t i = tid; i < R * per_row; i += nth) {
+      const int64_t r = i / per_row, c = i - r * per_row;
+      uint32_t w0[8];
+      ld256(base + (r * ld * esz) + 32 * c, w0);
+      absmax_words(w0, dtype, m, bad);
+    }
+  }
+  float f = dtype == Q2_BF16 ? __uint_as_float(max(m & 0xFFFFu, m >> 16) << 16) : __uint_as_float(m);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  for (int o = 16; o > 0; o >>= 1) f = fmaxf(f, __shfl_xor_sync(0xFFFFFFFFu, f, o));
   bad = __any_sync(0xFFFFFFFFu, bad);
   if ((threadIdx.x & 31) == 0) {
-    if (m > 0.f) atomicMax(amax_bits, __float_as_uint(m));
+    if (f > 0.f) atomicMax(amax_bits, __float_as_uint(f));
     if (bad) atomic_or_err(err, Q2_ERR_NONFINITE);
   }
 }
 
-// One thread per 16-group.  ncaps in {1, 2}.
-__global__ void __launch_bounds__(256) quant_fwd_kernel(
-    const void* __restrict__ x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,
-    double cap0, double cap1, double scale_div, const uint32_t* __restrict__ amax_bits,
-    uint8_t* __restrict__ codes, uint8_t* __restrict__ sf, float* __restrict__ scale32_out,
-    uint32_t* __restrict__ err) {
-  const int64_t gpr = K / GROUP, total = R * gpr, kb64 = kblocks64(K);
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const float amax = __uint_as_float(*amax_bits);
-  const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
-  if (gid == 0) *scale32_out = scale32;
-  if (gid >= total) return;
-  const int64_t r = gid / gpr, j = gid - r * gpr;
-  uint8_t* cout = codes + r * (K / 2) + j * 8;
-  uint8_t* sfout = sf + sf_offset(r, j, kb64);
-  if (amax == 0.f) {                                          // quantizers.py:219-220
-    *reinterpret_cast<uint2*>(cout) = make_uint2(0u, 0u);
-    *sfout = 0;
-    return;
-  }
-  float v[16];
-  load_vec8(x, dtype, r * ld + j * GROUP, v);
-  load_vec8(x, dtype, r * ld + j * GROUP + 8, v + 8);
-  float gmax = 0.f;
-#pragma unroll
+// Literal float64 restatement for one 16-group (the certified fallback of the
+// fast path and the reference semantics): exact threshold codes, sequential
+// float64 error, strict-less 4/6 selection.
+template <int DT>
+__device__ __forceinline__ uint3 quant_group_exact(const void* x, int64_t off, float scale32, int ncaps, double cap0,
+                                                double cap1, uint32_t* err) {
+  float v[16], gmax = 0.f;
+  load_vec8(x, DT, off, v);
+  load_vec8(x, DT, off + 8, v + 8);
   for (int k = 0; k < 16; ++k) gmax = fmaxf(gmax, fabsf(v[k]));
-
   const double s32 = (double)scale32;
   const double tq[7] = {0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0};
   uint32_t best_s8 = 0, best_lo = 0, best_hi = 0;
@@ -96,15 +116,13 @@ __global__ void __launch_bounds__(256) quant_fwd_kernel(
   for (int b = 0; b < ncaps; ++b) {
     const double c = b == 0 ? cap0 : cap1;
     const double xq = __ddiv_rn((double)gmax, __dmul_rn(s32, c));
-    if (isnan(xq)) atomic_or_err(err, Q2_ERR_NAN_SCALE);     // formats.py:167-168
+    if (isnan(xq)) atomic_or_err(err, Q2_ERR_NAN_SCALE);      // formats.py:167-168
     const uint32_t s8 = isnan(xq) ? 0u : e4m3_rtn(xq);
     const double d = __dmul_rn(e4m3_val(s8), s32);
     double T[7];
-#pragma unroll
     for (int t = 0; t < 7; ++t) T[t] = __dmul_rn(tq[t], d);
     uint32_t lo = 0, hi = 0;
     double e = 0.0;
-#pragma unroll
     for (int k = 0; k < 16; ++k) {
       const double a = fabs((double)v[k]);
       uint32_t mag = 0, neg = 0;
@@ -125,8 +143,270 @@ __global__ void __launch_bounds__(256) quant_fwd_kernel(
       best_err = e; best_s8 = s8; best_lo = lo; best_hi = hi;
     }
   }
-  *reinterpret_cast<uint2*>(cout) = make_uint2(best_lo, best_hi);
-  *sfout = (uint8_t)best_s8;
+  return make_uint3(best_lo, best_hi, best_s8);
+}
+
+// ---------------------------------------------------------------- fast path --
+// E4M3 value of a code 0..126 as float (exact).
+__device__ __forceinline__ float e4m3_valf(uint32_t k) {
+  return k < 8 ? (float)k * 0x1p-9f : __uint_as_float((((k >> 3) + 120u) << 23) | ((k & 7u) << 20));
+}
+__device__ __forceinline__ uint32_t cvt_e4m3_rn(float y) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %1;" : "=h"(r) : "f"(y));
+  return r & 0xFFu;
+}
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// Eight elements (four packed pairs) of one branch: E2M1 codes of the lower and
+// upper quotient brackets (rz products with inv(1-eps), inv(1+eps)) as two
+// 32-bit words, and the residuals rho - q_lo of the lower-bracket codes.
+__device__ __forceinline__ void branch8(const uint64_t (&vv)[4], uint64_t ilo, uint64_t ihi, uint32_t& wlo,
+                                        uint32_t& whi, float (&e)[8]) {
+  asm("{\n\t"
+      ".reg .b64 l0, l1, l2, l3, h0, h1, h2, h3;\n\t"
+      ".reg .b8 a0, a1, a2, a3, b0, b1, b2, b3;\n\t"
+      ".reg .f32 x0, x1, x2, x3, x4, x5, x6, x7;\n\t"
+      ".reg .b32 u0, u1, u2, u3;\n\t"
+      ".reg .f16 r0, r1, r2, r3, r4, r5, r6, r7;\n\t"
+      "mul.rz.f32x2 l0, %10, %14;\n\tmul.rz.f32x2 l1, %11, %14;\n\t"
+      "mul.rz.f32x2 l2, %12, %14;\n\tmul.rz.f32x2 l3, %13, %14;\n\t"
+      "mul.rz.f32x2 h0, %10, %15;\n\tmul.rz.f32x2 h1, %11, %15;\n\t"
+      "mul.rz.f32x2 h2, %12, %15;\n\tmul.rz.f32x2 h3, %13, %15;\n\t"
+      "mov.b64 {x0, x1}, l0;\n\tmov.b64 {x2, x3}, l1;\n\tmov.b64 {x4, x5}, l2;\n\tmov.b64 {x6, x7}, l3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 a0, x1, x0;\n\tcvt.rn.satfinite.e2m1x2.f32 a1, x3, x2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 a2, x5, x4;\n\tcvt.rn.satfinite.e2m1x2.f32 a3, x7, x6;\n\t"
+      "mov.b32 %0, {a0, a1, a2, a3};\n\t"
+      "{\n\t.reg .f32 y0, y1, y2, y3, y4, y5, y6, y7;\n\t"
+      "mov.b64 {y0, y1}, h0;\n\tmov.b64 {y2, y3}, h1;\n\tmov.b64 {y4, y5}, h2;\n\tmov.b64 {y6, y7}, h3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, y1, y0;\n\tcvt.rn.satfinite.e2m1x2.f32 b1, y3, y2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, y5, y4;\n\tcvt.rn.satfinite.e2m1x2.f32 b3, y7, y6;\n\t"
+      "mov.b32 %1, {b0, b1, b2, b3};\n\t}\n\t"
+      "cvt.rn.f16x2.e2m1x2 u0, a0;\n\tcvt.rn.f16x2.e2m1x2 u1, a1;\n\t"
+      "cvt.rn.f16x2.e2m1x2 u2, a2;\n\tcvt.rn.f16x2.e2m1x2 u3, a3;\n\t"
+      "mov.b32 {r0, r1}, u0;\n\tmov.b32 {r2, r3}, u1;\n\tmov.b32 {r4, r5}, u2;\n\tmov.b32 {r6, r7}, u3;\n\t"
+      "sub.rn.f32.f16 %2, r0, x0;\n\tsub.rn.f32.f16 %3, r1, x1;\n\t"
+      "sub.rn.f32.f16 %4, r2, x2;\n\tsub.rn.f32.f16 %5, r3, x3;\n\t"
+      "sub.rn.f32.f16 %6, r4, x4;\n\tsub.rn.f32.f16 %7, r5, x5;\n\t"
+      "sub.rn.f32.f16 %8, r6, x6;\n\tsub.rn.f32.f16 %9, r7, x7;\n\t"
+      "}"
+      : "=r"(wlo), "=r"(whi), "=f"(e[0]), "=f"(e[1]), "=f"(e[2]), "=f"(e[3]), "=f"(e[4]), "=f"(e[5]), "=f"(e[6]),
+        "=f"(e[7])
+      : "l"(vv[0]), "l"(vv[1]), "l"(vv[2]), "l"(vv[3]), "l"(ilo), "l"(ihi));
+}
+
+__device__ __forceinline__ void ffma2_acc(uint64_t& acc, float a, float b) {
+  const uint64_t p = pack2(a, b);
+  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(acc) : "l"(p));
+}
+__device__ __forceinline__ float hsum2(uint64_t acc) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(acc));
+  return a + b;
+}
+
+// Per-branch constants.  The E4M3 group scale is the hardware RTN candidate,
+// certified in fp32 against the two neighbouring midpoints (y = gmax/D has
+// relative error < 2^-22); uncertain groups go to the exact fix-up.
+struct BranchConst {
+  uint32_t s8;
+  float E, inv;
+  uint64_t ilo, ihi;
+  bool bad;
+};
+
+__device__ __forceinline__ BranchConst branch_const(float gmax, float invD, float s32f, const float* mids) {
+  BranchConst c;
+  const float y = gmax * invD;
+  c.s8 = cvt_e4m3_rn(y);
+  const float mlo = c.s8 > 0 ? mids[c.s8 - 1] : -1.f, mhi = mids[c.s8];   // mids[126] = +inf
+  c.bad = !(y > mlo * (1.0f + 0x1p-20f)) | !(y < mhi * (1.0f - 0x1p-20f));
+  c.E = e4m3_valf(c.s8);
+  const float d32 = c.E * s32f;                     // relative error <= 2^-24 vs E*scale32
+  c.bad |= !(d32 >= 0x1p-125f);
+  float inv;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d32));
+  c.inv = inv;
+  const float lo = inv * (1.0f - 0x1p-19f), hi = inv * (1.0f + 0x1p-19f);
+  c.ilo = pack2(lo, lo);
+  c.ihi = pack2(hi, hi);
+  return c;
+}
+
+// One branch over the 16 elements: codes, certification, S = sum (rho - q)^2.
+__device__ __forceinline__ void run_branch(const uint64_t (&vv)[8], const BranchConst& c, uint32_t& lo, uint32_t& hi,
+                                           bool& unc, float& S) {
+  uint32_t l2, h2;
+  float e[8];
+  uint64_t acc = 0;
+  const uint64_t (&va)[4] = *reinterpret_cast<const uint64_t(*)[4]>(&vv[0]);
+  const uint64_t (&vb)[4] = *reinterpret_cast<const uint64_t(*)[4]>(&vv[4]);
+  branch8(va, c.ilo, c.ihi, lo, l2, e);
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) ffma2_acc(acc, e[k], e[k + 1]);
+  branch8(vb, c.ilo, c.ihi, hi, h2, e);
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) ffma2_acc(acc, e[k], e[k + 1]);
+  unc |= (lo != l2) | (hi != h2);
+  S = hsum2(acc);
+}
+
+// |S - S*| bound: q has relative error <= 2^-18 (bracket + rcp.approx + rz), so
+// by Cauchy-Schwarz sum 2|e|d <= 2^-17 sqrt(S Q); FFMA accumulation adds 2^-20 S.
+__device__ __forceinline__ float s_bound(float S, float Q) {
+  return 0x1p-17f * 1.01f * sqrtf(S * Q) + 0x1p-35f * Q + 0x1p-20f * S;
+}
+
+// Persistent quantizer: a producer warp streams units of QT contiguous
+// 16-groups into a QNST-deep shared-memory ring with cp.async.bulk (TMA
+// engine); QT consumer threads quantize one group each per unit.  Fast path:
+// certified fp32 decisions (interval-checked E2M1 codes, bounded 4/6 error
+// comparison); uncertain groups run quant_group_exact.
+constexpr int QT = 256, QNST = 4;
+
+template <int DT>
+__global__ void __launch_bounds__(QT + 32, 2) quant_fwd_kernel(
+    const void* __restrict__ x, int64_t R, int64_t K, int ncaps, double cap0, double cap1, double scale_div,
+    FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+    float* __restrict__ scale32_out, uint32_t* __restrict__ fix_count, uint32_t* __restrict__ fix_list) {
+  constexpr int GB = DT == Q2_BF16 ? 32 : 64;               // bytes per 16-group
+  extern __shared__ __align__(128) unsigned char qsm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qsm + QNST * QT * GB);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + QNST);
+  const int64_t gpr = K / GROUP, total = R * gpr, kb64 = kblocks64(K);
+  const int64_t nunits = (total + QT - 1) / QT;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < QNST; ++s) { mbar_init(full0 + 8 * s, 1); mbar_init(empty0 + 8 * s, QT / 32); }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp == QT / 32) {                                      // producer warp
+    if ((threadIdx.x & 31) == 0) {
+      int i = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+        const int s = i % QNST;
+        if (i >= QNST) mbar_wait(empty0 + 8 * s, ((i / QNST) - 1) & 1);
+        const uint32_t bytes = (uint32_t)((total - u * QT < QT ? total - u * QT : QT) * GB);
+        mbar_expect_tx(full0 + 8 * s, bytes);
+        bulk_load(smem_u32(qsm + s * QT * GB), static_cast<const char*>(x) + u * QT * GB, bytes, full0 + 8 * s);
+      }
+    }
+    return;
+  }
+  const float amax = __uint_as_float(*amax_bits);
+  const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale32_out = scale32;
+  const double s32 = (double)scale32;
+  const double D0 = __dmul_rn(s32, cap0), D1 = __dmul_rn(s32, cap1);
+  const float invD0 = (float)(1.0 / D0), invD1 = (float)(1.0 / D1);
+  const float s32f = scale32;
+  const bool fast_ok = scale32 >= 0x1p-100f;                  // every d and 1/d stays normal in fp32
+  float* mids = reinterpret_cast<float*>(qsm + QNST * QT * GB + 128);
+  if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
+  asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+  int i = 0;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+    const int s = i % QNST;
+    mbar_wait(full0 + 8 * s, (i / QNST) & 1);
+    const int64_t gid = u * QT + threadIdx.x;
+    const bool live = gid < total;
+    uint32_t w[16];
+    if (live) {
+      const uint4* src = reinterpret_cast<const uint4*>(qsm + s * QT * GB + threadIdx.x * GB);
+#pragma unroll
+      for (int q = 0; q < GB / 16; ++q) {
+        const uint4 t = src[q];
+        w[4 * q] = t.x; w[4 * q + 1] = t.y; w[4 * q + 2] = t.z; w[4 * q + 3] = t.w;
+      }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(empty0 + 8 * s);  // slot may be refilled
+    if (!live) continue;
+    const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+    uint64_t vv[8];
+    float gmax;
+    uint64_t vacc = 0;
+    if (DT == Q2_BF16) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t t = w[k] & 0x7FFF7FFFu;
+        asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(t));
+        vv[k] = pack2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
+      }
+      gmax = __uint_as_float(max(m & 0xFFFFu, m >> 16) << 16);
+    } else {
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        m = max(m, max(w[2 * k] & 0x7FFFFFFFu, w[2 * k + 1] & 0x7FFFFFFFu));
+        vv[k] = pack2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1]));
+      }
+      gmax = __uint_as_float(m);
+    }
+    uint32_t lo = 0, hi = 0, s8 = 0;
+    bool exact = !fast_ok;
+    if (amax == 0.f) {
+      exact = false;                                          // quantizers.py:219-220
+    } else if (gmax == 0.f && fast_ok) {
+      // all-zero group: codes 0 (q = +0 since d = 0), scale 0, both errors 0
+    } else if (!exact) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(vacc) : "l"(vv[k]));
+      const float V = hsum2(vacc);
+      const BranchConst c0 = branch_const(gmax, invD0, s32f, mids);
+      bool unc = c0.bad;
+      float S0;
+      uint32_t lo0, hi0;
+      run_branch(vv, c0, lo0, hi0, unc, S0);
+      if (ncaps == 1) {
+        exact = unc;
+        lo = lo0; hi = hi0; s8 = c0.s8;
+      } else {
+        const BranchConst c1 = branch_const(gmax, invD1, s32f, mids);
+        unc |= c1.bad;
+        float S1;
+        uint32_t lo1, hi1;
+        run_branch(vv, c1, lo1, hi1, unc, S1);
+        const float Q0 = V * c0.inv * c0.inv * 1.001f, Q1 = V * c1.inv * c1.inv * 1.001f;
+        const float E0 = c0.E * c0.E, E1 = c1.E * c1.E;
+        const float A0 = E0 * S0, A1 = E1 * S1;
+        const float M = E0 * s_bound(S0, Q0) + E1 * s_bound(S1, Q1) + 0x1p-22f * (A0 + A1);
+        const bool pick1 = A1 + M < A0, pick0 = A0 + M < A1;  // strict: ties keep caps[0]
+        exact = unc || !(pick0 || pick1);
+        lo = pick1 ? lo1 : lo0; hi = pick1 ? hi1 : hi0; s8 = pick1 ? c1.s8 : c0.s8;
+      }
+    }
+    if (exact) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)gid;   // resolved by quant_fix_kernel
+    *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
+    sf[sf_offset(r, j, kb64)] = (uint8_t)s8;
+  }
+}
+
+// Exact float64 resolution of the groups the fast path could not certify.
+template <int DT>
+__global__ void __launch_bounds__(128) quant_fix_kernel(const void* __restrict__ x, int64_t K, int ncaps, double cap0,
+                                                        double cap1, double scale_div, FastDiv fgpr,
+                                                        const uint32_t* __restrict__ amax_bits,
+                                                        const uint32_t* __restrict__ fix_count,
+                                                        const uint32_t* __restrict__ fix_list, uint8_t* __restrict__ codes,
+                                                        uint8_t* __restrict__ sf, uint32_t* __restrict__ err) {
+  const uint32_t n = *fix_count;
+  const float amax = __uint_as_float(*amax_bits);
+  const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
+  const int64_t gpr = K / GROUP, kb64 = kblocks64(K);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t gid = fix_list[i];
+    const uint32_t r = fgpr.div(gid), j = gid - r * (uint32_t)gpr;
+    const uint3 e = quant_group_exact<DT>(x, (int64_t)gid * GROUP, scale32, ncaps, cap0, cap1, err);
+    *reinterpret_cast<uint2*>(codes + (int64_t)gid * 8) = make_uint2(e.x, e.y);
+    sf[sf_offset(r, j, kb64)] = (uint8_t)e.z;
+  }
 }
 
 }  // namespace q2
@@ -145,17 +425,18 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
                        uint32_t* amax_bits, uint32_t* err, void* stream) {
   if (!x || R < 0 || K % 16 || ld < K || (dtype != Q2_BF16 && dtype != Q2_F32)) return Q2_EINVAL;
   const int esz = dtype == Q2_BF16 ? 2 : 4;
-  if (!aligned16(x) || (ld * esz) % 16) return Q2_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(x) & 31u) || (ld * esz) % 32) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int64_t vecs = R * (K / 8);
-  int blocks = (int)std::min<int64_t>((vecs + 255) / 256, 148 * 16);
+  int blocks = (int)std::min<int64_t>((vecs + 255) / 256, 148 * 8);
   if (blocks < 1) blocks = 1;
   amax_kernel<<<blocks, 256, 0, s>>>(x, dtype, R, K, ld, amax_bits, err);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
 }
 
-extern "C" size_t q2_quant_fwd_ws_bytes(void) { return 16; }
+// ws: [0] amax bits, [1] fix-up count, [4..] fix-up list (one u32 per group).
+extern "C" size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K) { return 16 + 4 * (size_t)R * (size_t)(K / 16); }
 
 extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,
                             double cap0, double cap1, double scale_div, const q2_nvfp4* out,
@@ -163,14 +444,38 @@ extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int6
   if (!out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint32_t* amax = static_cast<uint32_t*>(ws);
-  if (cudaMemsetAsync(amax, 0, 4, s) != cudaSuccess) return Q2_ECUDA;
+  uint32_t* fix_count = amax + 1;
+  uint32_t* fix_list = amax + 4;
+  if (cudaMemsetAsync(amax, 0, 8, s) != cudaSuccess) return Q2_ECUDA;
   int rc = q2_amax(x, dtype, R, K, ld, amax, err, stream);
   if (rc) return rc;
-  int64_t groups = R * (K / 16);
-  int64_t blocks = (groups + 255) / 256;
-  if (blocks < 1) blocks = 1;
-  quant_fwd_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, dtype, R, K, ld, ncaps, cap0, cap1, scale_div,
-                                                   amax, out->codes, out->sf, out->scale32, err);
+  // The quantize pass streams contiguous rows (the host wrapper makes views contiguous).
+  if (ld != K || (reinterpret_cast<uintptr_t>(x) & 15u) || K / 16 >= (1ll << 31) || R * (K / 16) >= (1ll << 31))
+    return Q2_EINVAL;
+  const int64_t groups = R * (K / 16);
+  const int64_t units = (groups + QT - 1) / QT;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, 2 * nsm));
+  const FastDiv fg((uint32_t)(K / 16));
+  if (dtype == Q2_BF16) {
+    const int smem = QNST * QT * 32 + 128 + 512;
+    static bool a0 = false;
+    if (!a0) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a0 = true; }
+    quant_fwd_kernel<Q2_BF16><<<blocks, QT + 32, smem, s>>>(x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
+                                                             out->codes, out->sf, out->scale32, fix_count, fix_list);
+    quant_fix_kernel<Q2_BF16><<<2 * nsm, 128, 0, s>>>(x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+                                                      fix_list, out->codes, out->sf, err);
+  } else {
+    const int smem = QNST * QT * 64 + 128 + 512;
+    static bool a1 = false;
+    if (!a1) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a1 = true; }
+    quant_fwd_kernel<Q2_F32><<<blocks, QT + 32, smem, s>>>(x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
+                                                            out->codes, out->sf, out->scale32, fix_count, fix_list);
+    quant_fix_kernel<Q2_F32><<<2 * nsm, 128, 0, s>>>(x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+                                                     fix_list, out->codes, out->sf, err);
+  }
   Q2_CHECK_LAUNCH();
   return Q2_OK;
 }

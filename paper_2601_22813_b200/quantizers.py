@@ -189,7 +189,7 @@ def _quant_fwd(x, caps, scale_div, err=None) -> NVFP4Tensor:
     own = err is None
     if own:
         err = _err_word(x2.device)
-    ws = torch.empty(16, dtype=torch.uint8, device=x2.device)
+    ws = torch.empty(_lib.lib().q2_quant_fwd_ws_bytes(x2.shape[0], x2.shape[1]), dtype=torch.uint8, device=x2.device)
     t = out.c()
     c1 = float(caps[1]) if len(caps) > 1 else 0.0
     _lib.check(_lib.lib().q2_quant_fwd(x2.data_ptr(), dt, x2.shape[0], x2.shape[1], x2.shape[1], len(caps),
