@@ -38,10 +38,17 @@ __device__ __forceinline__ float fp4_valf(uint32_t code) {
 // ------------------------------------------------------------------ E4M3 ----
 // Decode a non-negative E4M3 code (0..126) (formats.py:53-66).
 __host__ __device__ __forceinline__ double e4m3_val(uint32_t code) {
-  uint32_t e = (code >> 3) & 0xF, m = code & 7;
+  const uint32_t e = (code >> 3) & 0xF, m = code & 7;
   if (e == 0) return (double)m * 0x1p-9;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)((((uint64_t)(e + 1016)) << 52) | ((uint64_t)m << 49)));
+#else
   return (double)(8 + m) * ldexp(1.0, (int)e - 10);
+#endif
 }
+// Bit-level helpers for positive normal doubles (no libm calls on the hot path).
+__device__ __forceinline__ int dexp(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7FF) - 1023; }
+__device__ __forceinline__ double dpow2(int e) { return __longlong_as_double((long long)((uint64_t)(e + 1023) << 52)); }
 
 // Nearest E4M3 code, ties to the even code, saturating at 448 (code 126).
 // Restates formats._nearest_even_index over the 126 exact midpoints
@@ -49,8 +56,8 @@ __host__ __device__ __forceinline__ double e4m3_val(uint32_t code) {
 __device__ __forceinline__ uint32_t e4m3_rtn(double x) {
   if (!(x < 432.0)) return 126u;                       // 432 is the top midpoint (tie -> 126, even)
   if (x < 0x1p-6) return (uint32_t)rint(x * 512.0);    // subnormal spacing 2^-9, rint = RNE
-  int e = ilogb(x);                                    // x in [2^e, 2^(e+1)), e in [-6, 8]
-  double f = __dsub_rn(ldexp(x, -e), 1.0);             // exact
+  const int e = dexp(x);                               // x in [2^e, 2^(e+1)), e in [-6, 8]
+  const double f = __dsub_rn(__dmul_rn(x, dpow2(-e)), 1.0);   // exact
   uint32_t q = (uint32_t)rint(f * 8.0);                // RNE on the mantissa; q == 8 carries
   uint32_t code = ((uint32_t)(e + 7) << 3) + q;
   return code > 126u ? 126u : code;
@@ -60,8 +67,8 @@ __device__ __forceinline__ uint32_t e4m3_rtn(double x) {
 __device__ __forceinline__ uint32_t e4m3_sr(double x, double u) {
   if (x < 0x1p-6) return e4m3_rtn(x);
   x = fmin(x, 448.0);
-  int e = ilogb(x);
-  double f = __dsub_rn(ldexp(x, -e), 1.0);
+  const int e = dexp(x);
+  const double f = __dsub_rn(__dmul_rn(x, dpow2(-e)), 1.0);
   uint32_t lo = ((uint32_t)(e + 7) << 3) + (uint32_t)floor(f * 8.0);
   if (lo > 125u) lo = 125u;
   double a = e4m3_val(lo), b = e4m3_val(lo + 1);
@@ -73,12 +80,12 @@ __device__ __forceinline__ uint32_t e4m3_sr(double x, double u) {
 // (formats.py:204-229).  Sets *ovf on overflow.
 __device__ __forceinline__ double e8m3_rtn(double x, bool* ovf) {
   if (x < 0x1p-126) return (x <= 0x1p-127) ? 0.0 : 0x1p-126;
-  int e;
-  double m = frexp(x, &e);                // m in [0.5, 1)
+  int e = dexp(x) + 1;                    // frexp: x = m 2^e, m in [0.5, 1)
+  const double m = __dmul_rn(x, dpow2(-e));
   double q = rint(16.0 * m);
   if (q >= 16.0) { q = 8.0; e += 1; }
-  if (e - 1 > 127) *ovf = true;
-  return ldexp(q / 16.0, e);
+  if (e - 1 > 127) { *ovf = true; return x; }
+  return __dmul_rn(q * 0.0625, dpow2(e));
 }
 
 // ------------------------------------------------------------ element RTN ---

@@ -526,7 +526,7 @@ static int fill_args(MsedArgs& a, const void* x, int dtype, const q2_nvfp4* tape
 
 template <int SRC, int DT>
 static int launch_fast1(const MsedArgs& a, const FastArgs& f, cudaStream_t st) {
-  const int smem = F_ROWS * (DT == Q2_BF16 ? 256 : 512) + 256;
+  const int smem = F_ROWS * (DT == Q2_BF16 ? 256 : 512) + 256 + 64;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(msed_fast1_kernel<SRC, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)

@@ -31,52 +31,69 @@ __device__ __forceinline__ int f_swz(int row) { return (row & 7) ^ ((row >> 3) &
 // Stage the tile (signs applied) as bf16 (DT == Q2_BF16, tape) or fp32.
 template <int SRC, int DT>
 __device__ __forceinline__ void fast_load_tile(const MsedArgs& a, int64_t r0, int64_t c, unsigned char* tile,
-                                               const uint32_t* sgnw, bool& bad) {
+                                               const uint32_t* sgnw, bool& bad, int* espan) {
   const int t = threadIdx.x;
   constexpr int ROWB = DT == Q2_BF16 ? 256 : 512;       // bytes per staged row
   if (SRC == Q2_SRC_ROWS) {
     constexpr int SEGS = ROWB / 16;
-    for (int v = t; v < F_ROWS * SEGS; v += F_THREADS) {
-      const int rr = v / SEGS, sg = v % SEGS;
-      uint4 q = make_uint4(0, 0, 0, 0);
+    constexpr int NV = F_ROWS * SEGS / F_THREADS;
+    uint4 q[NV];
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {                      // issue every load first
+      const int v = t + it * F_THREADS, rr = v / SEGS, sg = v % SEGS;
+      q[it] = make_uint4(0, 0, 0, 0);
       if (r0 + rr < a.R) {
         const char* src = static_cast<const char*>(a.x) + ((r0 + rr) * a.ld + c * CHUNK) * (DT == Q2_BF16 ? 2 : 4);
-        q = __ldg(reinterpret_cast<const uint4*>(src) + sg);
+        q[it] = __ldg(reinterpret_cast<const uint4*>(src) + sg);
       }
+    }
+    uint32_t m16 = 0, m32 = 0;
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {
+      const int v = t + it * F_THREADS, rr = v / SEGS, sg = v % SEGS;
+      uint4 w = q[it];
       if (DT == Q2_BF16) {                               // 8 elements: positions 8sg .. 8sg+7
         const uint4 m = *reinterpret_cast<const uint4*>(sgnw + 4 * sg);
-        q.x ^= m.x; q.y ^= m.y; q.z ^= m.z; q.w ^= m.w;
-        const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
+        w.x ^= m.x; w.y ^= m.y; w.z ^= m.z; w.w ^= m.w;
+        const uint32_t ww[4] = {w.x & 0x7FFF7FFFu, w.y & 0x7FFF7FFFu, w.z & 0x7FFF7FFFu, w.w & 0x7FFF7FFFu};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          bad |= ((ww[i] & 0x7F80u) == 0x7F80u) | ((ww[i] & 0x7F800000u) == 0x7F800000u);
+        for (int i = 0; i < 4; ++i) asm("max.u16x2 %0, %0, %1;" : "+r"(m16) : "r"(ww[i]));
       } else {                                           // 4 elements: positions 4sg .. 4sg+3
         const uint32_t bits = (a.sign[sg >> 3] >> ((4 * sg) & 31)) & 0xF;
-        q.x ^= (bits & 1) << 31; q.y ^= ((bits >> 1) & 1) << 31;
-        q.z ^= ((bits >> 2) & 1) << 31; q.w ^= ((bits >> 3) & 1) << 31;
-        bad |= ((q.x & 0x7F800000u) == 0x7F800000u) | ((q.y & 0x7F800000u) == 0x7F800000u) |
-               ((q.z & 0x7F800000u) == 0x7F800000u) | ((q.w & 0x7F800000u) == 0x7F800000u);
+        w.x ^= (bits & 1) << 31; w.y ^= ((bits >> 1) & 1) << 31;
+        w.z ^= ((bits >> 2) & 1) << 31; w.w ^= ((bits >> 3) & 1) << 31;
+        m32 = max(m32, max(max(w.x & 0x7FFFFFFFu, w.y & 0x7FFFFFFFu), max(w.z & 0x7FFFFFFFu, w.w & 0x7FFFFFFFu)));
       }
-      *reinterpret_cast<uint4*>(tile + rr * ROWB + ((sg ^ f_swz(rr)) << 4)) = q;
+      *reinterpret_cast<uint4*>(tile + rr * ROWB + ((sg ^ f_swz(rr)) << 4)) = w;
     }
+    bad |= (m16 & 0xFFFFu) >= 0x7F80u || (m16 >> 16) >= 0x7F80u || m32 >= 0x7F800000u;
   } else if (SRC == Q2_SRC_COLS) {
     // source [K, R]: a 16-byte source segment holds 8 (bf16) / 4 (fp32) tile rows at one k
     constexpr int EPS = DT == Q2_BF16 ? 8 : 4;
     constexpr int CSEG = F_ROWS / EPS;
-    for (int v = t; v < CHUNK * CSEG; v += F_THREADS) {
-      const int kk = v / CSEG, cs = v % CSEG;
-      uint4 q = make_uint4(0, 0, 0, 0);
+    constexpr int NV = CHUNK * CSEG / F_THREADS;
+    uint4 q[NV];
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {
+      const int v = t + it * F_THREADS, kk = v / CSEG, cs = v % CSEG;
+      q[it] = make_uint4(0, 0, 0, 0);
       if (r0 + cs * EPS < a.R) {
         const char* src = static_cast<const char*>(a.x) + ((c * CHUNK + kk) * a.ld + r0 + cs * EPS) * (DT == Q2_BF16 ? 2 : 4);
-        q = __ldg(reinterpret_cast<const uint4*>(src));
+        q[it] = __ldg(reinterpret_cast<const uint4*>(src));
       }
+    }
+    uint32_t m16 = 0, m32 = 0;
+#pragma unroll
+    for (int it = 0; it < NV; ++it) {
+      const int v = t + it * F_THREADS, kk = v / CSEG, cs = v % CSEG;
       const bool neg = (a.sign[kk >> 5] >> (kk & 31)) & 1;
-      const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
+      const uint32_t ww[4] = {q[it].x, q[it].y, q[it].z, q[it].w};
       if (DT == Q2_BF16) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t w = ww[i] ^ (neg ? 0x80008000u : 0u);
-          bad |= ((w & 0x7F80u) == 0x7F80u) | ((w & 0x7F800000u) == 0x7F800000u);
+          const uint32_t aw = w & 0x7FFF7FFFu;
+          asm("max.u16x2 %0, %0, %1;" : "+r"(m16) : "r"(aw));
           const int ra = cs * 8 + 2 * i, rb = ra + 1;
           *reinterpret_cast<uint16_t*>(tile + ra * ROWB + (((kk >> 3) ^ f_swz(ra)) << 4) + (kk & 7) * 2) = (uint16_t)w;
           *reinterpret_cast<uint16_t*>(tile + rb * ROWB + (((kk >> 3) ^ f_swz(rb)) << 4) + (kk & 7) * 2) = (uint16_t)(w >> 16);
@@ -85,12 +102,13 @@ __device__ __forceinline__ void fast_load_tile(const MsedArgs& a, int64_t r0, in
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t w = ww[i] ^ (neg ? 0x80000000u : 0u);
-          bad |= (w & 0x7F800000u) == 0x7F800000u;
+          m32 = max(m32, w & 0x7FFFFFFFu);
           const int ra = cs * 4 + i;
           *reinterpret_cast<uint32_t*>(tile + ra * ROWB + (((kk >> 2) ^ f_swz(ra)) << 4) + (kk & 3) * 4) = w;
         }
       }
     }
+    bad |= (m16 & 0xFFFFu) >= 0x7F80u || (m16 >> 16) >= 0x7F80u || m32 >= 0x7F800000u;
   } else {
     // NVFP4 tape [K, R]: thread t decodes tape row k = t (64 codes + 4 scales), stores FP4*E4M3 as bf16 (exact)
     const int kk = t;
@@ -106,6 +124,21 @@ __device__ __forceinline__ void fast_load_tile(const MsedArgs& a, int64_t r0, in
       sfw = __ldg(reinterpret_cast<const uint32_t*>(a.tape_sf + sf_offset(trow, r0 / 16, kblocks64(a.R))));
     }
     const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    // exponent span of the nonzero group scales per column group: values are
+    // multiples of 2^(E_min-11) below 2^(E_max-3), so the fp32 Hadamard of the
+    // chunk is exact when E_max - E_min <= 9 (SURVEY E6 tape certificate).
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t s8 = (sfw >> (8 * q)) & 0xFF;
+      const int e = max(1, (int)(s8 >> 3));
+      int emin = s8 ? e : 64, emax = s8 ? e : -64;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+        emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
+      }
+      if ((t & 31) == 0) { atomicMin(&espan[2 * q], emin); atomicMax(&espan[2 * q + 1], emax); }
+    }
 #pragma unroll
     for (int i = 0; i < 64; ++i) {
       const uint32_t code = (w[i >> 3] >> (4 * (i & 7))) & 0xF;
@@ -163,13 +196,15 @@ __global__ void __launch_bounds__(F_THREADS, 4) msed_fast1_kernel(MsedArgs a, Fa
   unsigned char* tile = fsm;
   uint32_t* sgnw = reinterpret_cast<uint32_t*>(fsm + F_ROWS * ROWB);   // 64 bf16-pair sign words
   const int64_t r0 = (int64_t)blockIdx.x * F_ROWS, c = blockIdx.y;
+  int* espan = reinterpret_cast<int*>(fsm + F_ROWS * ROWB + 256);      // [4][min, max]
+  if (threadIdx.x < 8) espan[threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
   if (threadIdx.x < 64) {
     const int e = 2 * threadIdx.x;
     sgnw[threadIdx.x] = (((a.sign[e >> 5] >> (e & 31)) & 1u) << 15) | (((a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u) << 31);
   }
   __syncthreads();
   bool bad = false;
-  fast_load_tile<SRC, DT>(a, r0, c, tile, sgnw, bad);
+  fast_load_tile<SRC, DT>(a, r0, c, tile, sgnw, bad, espan);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomic_or_err(a.err, Q2_ERR_NONFINITE);
 
   const double c_eff = SRC == Q2_SRC_TAPE_COLS ? a.inv_sqrt * (double)*a.tape_scale32 : a.inv_sqrt;
@@ -231,7 +266,8 @@ __global__ void __launch_bounds__(F_THREADS, 4) msed_fast1_kernel(MsedArgs a, Fa
   f2unpack(acc, n0, n1);
   float num = n0 + n1;
   num += __shfl_xor_sync(0xFFFFFFFFu, num, 1);
-  const float eps = 7.0f * 0x1p-24f * 1.001f * sqrtf(num) + 0x1p-120f;   // sqrtf: <= 1 ulp
+  float eps = 7.0f * 0x1p-24f * 1.001f * sqrtf(num) + 0x1p-120f;   // sqrtf: <= 1 ulp
+  if (SRC == Q2_SRC_TAPE_COLS && espan[2 * (rr >> 4) + 1] - espan[2 * (rr >> 4)] <= 9) eps = 0.f;
   // ---- per group: pseudo-scale, codes, <y, rho>
   bool unc = !live;
   float den = 0.f, pmx = 0.f;
