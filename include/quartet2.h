@@ -22,11 +22,17 @@
  * NVFP4 tensor in HBM (q2_nvfp4): a logical [R, K] tensor quantized along K.
  *  codes   uint8 [R, K/2], row-major, two E2M1 codes per byte, low nibble =
  *          even k (the NV4T packing of quantizers.py:339).
- *  sf      UE4M3 group scales (one per 16 along K) in the tcgen05 block-scale
- *          atom layout: 512-byte atoms of 128 rows x 4 scales, atoms K-fastest,
- *          rows padded to a multiple of 128 with zero scales.  Byte of (r, j):
- *            ((r/128)*ceil(K/64) + j/4)*512 + (r%32)*16 + ((r%128)/32)*4 + j%4
- *          Size: q2_sf_bytes(R, K).
+ *  sf      UE4M3 group scales (one per 16 along K) stored as the TMEM image of a
+ *          tcgen05.cp.128x256b copy: one 4 KiB block per (128-row block, pair of
+ *          64-element K blocks), blocks K-fastest; rows padded to 128.  Block
+ *          row L (TMEM lane) = 32 B: for K block h of the pair, bytes 16h+4q+i
+ *          hold scale i of row 32q + L%32 (the MMA scale-vector layout, one
+ *          replica per 32-lane subpartition), stored core-matrix major.  The
+ *          primary byte of (r, j) is
+ *            ((r/128)*ceil(K/128) + j/8)*4096 + ((r%32)/8)*256 + ((j/4)%2)*128
+ *              + (r%8)*16 + ((r%128)/32)*4 + j%4
+ *          and its replicas sit +1024, +2048, +3072 bytes later.
+ *          Size: q2_sf_bytes(R, K) = ceil(R/128)*ceil(K/128)*4096.
  *  scale32 float32 device scalar (the reference's np.float32 tensor scale).
  */
 #ifndef QUARTET2_H_

@@ -15,12 +15,23 @@ constexpr int GROUP = 16;
 constexpr int CHUNK = 128;
 
 // ---------------------------------------------------------------- layout ----
-// Byte offset of scale (r, j) in the tcgen05 block-scale atom layout
-// (128x4 atoms of 512 B, K-fastest).  See include/quartet2.h.
-__host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t j, int64_t kb64) {
-  return (((r >> 7) * kb64 + (j >> 2)) << 9) + ((r & 31) << 4) + (((r >> 5) & 3) << 2) + (j & 3);
+// Group scales are stored as the TMEM image of a tcgen05.cp.128x256b copy:
+// one 4 KiB block per (128-row block, 128-column K pair), blocks K-fastest.
+// Block row L (= TMEM lane) holds 32 B = 8 TMEM columns: for K-block h of the
+// pair, columns 4h..4h+3 carry the four scales of rows 32q + L%32 (q = 0..3),
+// i.e. the MMA scale-vector layout with each 32-lane subpartition holding a
+// replica.  Stored core-matrix major (8 rows x 16 B) with LBO 128 B / SBO 256 B.
+// sf_offset returns the primary replica; replica t sits t*1024 bytes later.
+__host__ __device__ __forceinline__ int64_t kpairs(int64_t K) { return (K + 127) / 128; }
+__host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t j, int64_t kp) {
+  const int64_t L = r & 31;
+  return (((r >> 7) * kp + (j >> 3)) << 12) + ((L >> 3) << 8) + (((j >> 2) & 1) << 7) + ((L & 7) << 4) +
+         (((r >> 5) & 3) << 2) + (j & 3);
 }
-__host__ __device__ __forceinline__ int64_t kblocks64(int64_t K) { return (K + 63) / 64; }
+__device__ __forceinline__ void sf_store(uint8_t* sf, int64_t r, int64_t j, int64_t kp, uint8_t v) {
+  uint8_t* p = sf + sf_offset(r, j, kp);
+  p[0] = v; p[1024] = v; p[2048] = v; p[3072] = v;
+}
 
 // ------------------------------------------------------------------ E2M1 ----
 // magnitude code -> value (formats.py:43-46); code 8 is +0.

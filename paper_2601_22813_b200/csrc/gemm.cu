@@ -33,7 +33,7 @@ namespace q2 {
 constexpr int BM = 128, BN = 128, BKB = 128;             // BK = 256 fp4 = 128 bytes
 constexpr int A_STAGE = BM * BKB;                         // 16 KB
 constexpr int B_STAGE = BN * BKB;                         // 16 KB
-constexpr int SF_STAGE = 4 * 512;                         // 4 atoms (128 rows x 16 scales)
+constexpr int SF_STAGE = 2 * 4096;                        // two 128x256b TMEM-image blocks (K pairs)
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE + 2 * SF_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int SFA_COL = 256, SFB_COL = 272;               // after two 128-column accumulators
@@ -42,7 +42,7 @@ constexpr int GROUP_M = 8;
 
 template <bool F32>
 struct GemmCfg {
-  static constexpr int STAGES = F32 ? 4 : 5;
+  static constexpr int STAGES = F32 ? 3 : 4;
   static constexpr int OUT_BYTES = BM * BN * (F32 ? 4 : 2);          // staging for the TMA store
   static constexpr int OFF_OUT = STAGES * STAGE_BYTES;
   static constexpr int OFF_BAR = OFF_OUT + OUT_BYTES;
@@ -77,14 +77,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
-// tcgen05.cp source descriptor: 32 rows x 16 B, no swizzle, 8-row groups 128 B apart.
+// tcgen05.cp 128x256b source descriptor: core matrices of 8 rows x 16 B, the
+// two K halves 128 B apart (LBO), 8-row groups 256 B apart (SBO), no swizzle.
 __device__ __forceinline__ uint64_t desc_sf(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 32) | (1ull << 46);
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_cp_sf(uint32_t tmem, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem), "l"(desc) : "memory");
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem), "l"(desc) : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t tsfa, uint32_t tsfb, uint32_t accum) {
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nsub_total = g.K / 64;                   // K = 64 MMAs
   const int nk = (nsub_total + 3) / 4;
-  const int64_t kb64 = nsub_total;                   // scale atoms per 128-row block
+  const int64_t kpr = (g.K + 127) / 128;             // scale image blocks per 128-row block
   const int ntiles = g.tiles_m * g.tiles_n;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -175,15 +176,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kt = 0; kt < nk; ++kt, ++it) {
           const int s = it % C::STAGES;
           if (it >= C::STAGES) mbar_wait(bar_empty + 8 * s, ((it / C::STAGES) - 1) & 1);
-          const int nsub = min(4, nsub_total - kt * 4);
+          const int nkp = (int)(kpr - 2 * kt < 2 ? kpr - 2 * kt : 2);
           unsigned char* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(bar_full + 8 * s, A_STAGE + B_STAGE + 2 * nsub * 512);
+          mbar_expect_tx(bar_full + 8 * s, A_STAGE + B_STAGE + 2 * nkp * 4096);
           tma_load_2d(smem_u32(st), &tmA, kt * BKB, m0, bar_full + 8 * s);
           tma_load_2d(smem_u32(st + A_STAGE), &tmB, kt * BKB, n0, bar_full + 8 * s);
-          bulk_load(smem_u32(st + A_STAGE + B_STAGE), g.sfa + (((int64_t)tm * kb64 + kt * 4) << 9), nsub * 512,
+          bulk_load(smem_u32(st + A_STAGE + B_STAGE), g.sfa + (((int64_t)tm * kpr + 2 * kt) << 12), nkp * 4096,
                     bar_full + 8 * s);
-          bulk_load(smem_u32(st + A_STAGE + B_STAGE + SF_STAGE), g.sfb + (((int64_t)tn * kb64 + kt * 4) << 9),
-                    nsub * 512, bar_full + 8 * s);
+          bulk_load(smem_u32(st + A_STAGE + B_STAGE + SF_STAGE), g.sfb + (((int64_t)tn * kpr + 2 * kt) << 12),
+                    nkp * 4096, bar_full + 8 * s);
         }
       }
     }
@@ -202,9 +203,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const int nsub = min(4, nsub_total - kt * 4);
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          for (int kk = 0; kk < nsub; ++kk) {
-            tc_cp_sf(tmem + SFA_COL + 4 * kk, desc_sf(st + A_STAGE + B_STAGE + kk * 512));
-            tc_cp_sf(tmem + SFB_COL + 4 * kk, desc_sf(st + A_STAGE + B_STAGE + SF_STAGE + kk * 512));
+          for (int p = 0; p < (nsub + 1) / 2; ++p) {
+            tc_cp_sf(tmem + SFA_COL + 8 * p, desc_sf(st + A_STAGE + B_STAGE + p * 4096));
+            tc_cp_sf(tmem + SFB_COL + 8 * p, desc_sf(st + A_STAGE + B_STAGE + SF_STAGE + p * 4096));
           }
           const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_STAGE);
           for (int kk = 0; kk < nsub; ++kk)

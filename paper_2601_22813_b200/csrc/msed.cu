@@ -112,7 +112,7 @@ __device__ __forceinline__ void load_tile(const MsedArgs& a, int64_t r0, int64_t
       }
       uint4 raw = __ldg(reinterpret_cast<const uint4*>(a.tape_codes + trow * (a.R / 2) + tcol / 2));
       uint32_t sfw = __ldg(reinterpret_cast<const uint32_t*>(
-          a.tape_sf + sf_offset(trow, r0 / 16, kblocks64(a.R))));
+          a.tape_sf + sf_offset(trow, r0 / 16, kpairs(a.R))));
       uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(MSED_THREADS) msed_kernel(MsedArgs a) {
   double* scratch = reinterpret_cast<double*>(smem_raw + TILE_ROWS * TILE_LD * sizeof(float));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)blockIdx.x * TILE_ROWS, c = blockIdx.y;
-  const int64_t gpr = a.K / GROUP, kb64 = kblocks64(a.K);
+  const int64_t gpr = a.K / GROUP, kpr = kpairs(a.K);
 
   bool bad = false;
   load_tile<SRC>(a, r0, c, tile, bad);
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(MSED_THREADS) msed_kernel(MsedArgs a) {
     }
     if (zero) {                                                  // quantizers.py:175-176
       *reinterpret_cast<uint16_t*>(a.codes + r * (a.K / 2) + c * 64 + 2 * lane) = 0;
-      if ((lane & 3) == 0) a.sf[sf_offset(r, c * 8 + (lane >> 2), kb64)] = 0;
+      if ((lane & 3) == 0) sf_store(a.sf, r, c * 8 + (lane >> 2), kpr, 0);
       continue;
     }
     double d;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(MSED_THREADS) msed_kernel(MsedArgs a) {
     }
     *reinterpret_cast<uint16_t*>(a.codes + r * (a.K / 2) + c * 64 + 2 * lane) = (uint16_t)codes;
     if (PASS == PASS_QUANT && scale32 == 0.f) {                  // ms_eden.py:139-140
-      if ((lane & 3) == 0) a.sf[sf_offset(r, c * 8 + (lane >> 2), kb64)] = (uint8_t)s8;
+      if ((lane & 3) == 0) sf_store(a.sf, r, c * 8 + (lane >> 2), kpr, (uint8_t)s8);
       continue;
     }
     // EDEN factor S = <x,x>/<x,q> in numpy pairwise order (ms_eden.py:75-83)
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(MSED_THREADS) msed_kernel(MsedArgs a) {
       const double corrected = __dmul_rn(S, e4m3_val(s8));       // ms_eden.py:142-143
       if (corrected > 448.0) atomic_or_err(a.err, Q2_ERR_SCALE448);
       const double uu = prng_uniform(a.sr_head, (uint64_t)g);
-      a.sf[sf_offset(r, c * 8 + (lane >> 2), kb64)] = (uint8_t)e4m3_sr(fmin(corrected, 448.0), uu);
+      sf_store(a.sf, r, c * 8 + (lane >> 2), kpr, (uint8_t)e4m3_sr(fmin(corrected, 448.0), uu));
     }
   }
   if (PASS != PASS_QUANT) {
@@ -312,7 +312,7 @@ __device__ __forceinline__ void load_chunk_lit(const MsedArgs& a, int64_t r, int
     } else {
       const uint32_t byte = a.tape_codes[k * (a.R / 2) + r / 2];
       const uint32_t code = (r & 1) ? byte >> 4 : byte & 0xF;
-      const uint32_t s8 = a.tape_sf[sf_offset(k, r / 16, kblocks64(a.R))];
+      const uint32_t s8 = a.tape_sf[sf_offset(k, r / 16, kpairs(a.R))];
       v = __dmul_rn(__dmul_rn(fp4_val(code), e4m3_val(s8)), (double)*a.tape_scale32);
     }
     y[i] = ((a.sign[e >> 5] >> (e & 31)) & 1u) ? -v : v;
@@ -400,8 +400,8 @@ __global__ void posthoc2_cert_kernel(const uint16_t* __restrict__ pseudo, const 
   if (g == 0) *scale32_out = scale32;
   if (g >= total) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  uint8_t* out = sf + sf_offset(r, j, kblocks64(K));
-  if (pmax == 0.0) { *out = 0; return; }
+  const int64_t kpr = kpairs(K);
+  if (pmax == 0.0) { sf_store(sf, r, j, kpr, 0); return; }
   const double ps = (double)__uint_as_float((uint32_t)pseudo[g] << 16);
   const double shifted = __ddiv_rn(ps, (double)scale32);
   const int64_t ch = r * (K / CHUNK) + j / 8;
@@ -411,13 +411,13 @@ __global__ void posthoc2_cert_kernel(const uint16_t* __restrict__ pseudo, const 
   if (d == 0.f) {
     const double corrected = __dmul_rn(S, shifted);
     if (corrected > 448.0) atomic_or_err(err, Q2_ERR_SCALE448);
-    *out = (uint8_t)e4m3_sr(fmin(corrected, 448.0), u);
+    sf_store(sf, r, j, kpr, (uint8_t)e4m3_sr(fmin(corrected, 448.0), u));
     return;
   }
   const double cm = __dmul_rn(S, shifted);
   const double lo = cm * (1.0 - (double)d), hi = cm * (1.0 + (double)d);
   const uint32_t clo = e4m3_sr(fmin(lo, 448.0), u), chi = e4m3_sr(fmin(hi, 448.0), u);
-  if (clo == chi && hi <= 448.0 && d < 1e-3f) { *out = (uint8_t)clo; return; }
+  if (clo == chi && hi <= 448.0 && d < 1e-3f) { sf_store(sf, r, j, kpr, (uint8_t)clo); return; }
   listB[atomicAdd(listB_n, 1u)] = (uint32_t)g;
 }
 
@@ -441,8 +441,7 @@ __global__ void __launch_bounds__(128) posthoc_fix2_kernel(MsedArgs a, const uin
       const double ps = (double)__uint_as_float((uint32_t)a.pseudo[g] << 16);
       const double corrected = __dmul_rn(S, __ddiv_rn(ps, (double)scale32));
       if (corrected > 448.0) atomic_or_err(a.err, Q2_ERR_SCALE448);
-      a.sf[sf_offset(r, j, kblocks64(a.K))] =
-          (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g));
+      sf_store(a.sf, r, j, kpairs(a.K), (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g)));
     }
   }
 }
@@ -463,13 +462,13 @@ __global__ void posthoc2_kernel(const uint16_t* __restrict__ pseudo, const doubl
   if (g == 0) *scale32_out = scale32;
   if (g >= total) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  uint8_t* out = sf + sf_offset(r, j, kblocks64(K));
-  if (pmax == 0.0) { *out = 0; return; }
+  const int64_t kpr = kpairs(K);
+  if (pmax == 0.0) { sf_store(sf, r, j, kpr, 0); return; }
   const double ps = (double)__uint_as_float((uint32_t)pseudo[g] << 16);
   const double shifted = __ddiv_rn(ps, (double)scale32);
   const double corrected = __dmul_rn(corr[r * (K / CHUNK) + j / 8], shifted);
   if (corrected > 448.0) atomic_or_err(err, Q2_ERR_SCALE448);
-  *out = (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g));
+  sf_store(sf, r, j, kpr, (uint8_t)e4m3_sr(fmin(corrected, 448.0), prng_uniform(sr_head, (uint64_t)g)));
 }
 
 }  // namespace q2

@@ -121,7 +121,7 @@ __device__ __forceinline__ void fast_load_tile(const MsedArgs& a, int64_t r0, in
       const uint4* src = reinterpret_cast<const uint4*>(a.tape_codes + trow * (a.R / 2) + r0 / 2);
       q0 = __ldg(src);
       q1 = __ldg(src + 1);
-      sfw = __ldg(reinterpret_cast<const uint32_t*>(a.tape_sf + sf_offset(trow, r0 / 16, kblocks64(a.R))));
+      sfw = __ldg(reinterpret_cast<const uint32_t*>(a.tape_sf + sf_offset(trow, r0 / 16, kpairs(a.R))));
     }
     const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
     // exponent span of the nonzero group scales per column group: values are

@@ -27,10 +27,10 @@ def test_library_exports_header_symbols():
 def test_sf_bytes():
     from paper_2601_22813_b200 import _lib
     L = _lib.lib()
-    assert L.q2_sf_bytes(128, 64) == 512
-    assert L.q2_sf_bytes(129, 64) == 1024
-    assert L.q2_sf_bytes(128, 256) == 2048
-    assert L.q2_sf_bytes(256, 80) == 2 * 2 * 512
+    assert L.q2_sf_bytes(128, 64) == 4096
+    assert L.q2_sf_bytes(129, 64) == 8192
+    assert L.q2_sf_bytes(128, 256) == 8192
+    assert L.q2_sf_bytes(256, 80) == 2 * 4096
 
 
 def test_host_streams_match_oracle():
@@ -45,13 +45,33 @@ def test_host_streams_match_oracle():
 
 
 def test_sf_layout_formula():
-    """SF byte offsets match the CuTe blockscaled atom ((32,4),(16,4)):((16,4),(0,1))."""
+    """The scale image (include/quartet2.h) places every (row, group) at 4 distinct
+    replicas, covers each 4 KiB block exactly, and per TMEM lane L / column c holds
+    the scale of row 32*(c%4) + L%32 (the tcgen05 block-scale vector layout)."""
     def off(r, j, K):
-        kb = (K + 63) // 64
-        return ((r // 128) * kb + j // 4) * 512 + (r % 32) * 16 + ((r % 128) // 32) * 4 + j % 4
+        kp = (K + 127) // 128
+        L = r % 32
+        return (((r // 128) * kp + j // 8) * 4096 + (L // 8) * 256 + ((j // 4) % 2) * 128 + (L % 8) * 16
+                + ((r % 128) // 32) * 4 + j % 4)
     K, R = 256, 256
-    seen = {off(r, j, K) for r in range(R) for j in range(K // 16)}
-    assert len(seen) == R * K // 16 and max(seen) < R * K // 16
+    seen = set()
+    for r in range(R):
+        for j in range(K // 16):
+            for t in range(4):
+                seen.add(off(r, j, K) + 1024 * t)
+    assert len(seen) == 4 * R * K // 16 and max(seen) < 4 * R * K // 16
+    # lane view: block byte b -> (lane, column, byte-in-column) of a 128x256b copy
+    def lane_col(b):
+        g, rest = divmod(b % 4096, 256)
+        half, rest = divmod(rest, 128)
+        row8, byte = divmod(rest, 16)
+        return 8 * g + row8, 4 * half + byte // 4, byte % 4
+    for r in (0, 5, 37, 100, 127):
+        for j in (0, 3, 4, 7):
+            for t in range(4):
+                lane, col, i = lane_col(off(r, j, K) + 1024 * t)
+                assert lane % 32 == r % 32 and lane // 32 == t
+                assert col == 4 * ((j // 4) % 2) + (r % 128) // 32 and i == j % 4
 
 
 def test_layer_config_validation():
