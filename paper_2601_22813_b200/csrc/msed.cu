@@ -385,40 +385,79 @@ __device__ __forceinline__ float posthoc_scale32(double pmax) {
   return (float)ldexp(1.0, (m == 0.5) ? e - 1 : e);         // ms_eden.py:86-91
 }
 
-// Certified pass 2 (posthoc.py:98-125): one thread per group; the SR decision
-// must agree at both ends of corr * (1 -+ dS), else the group is re-done by
-// posthoc_fix2_kernel with the exact float64 factor.
-__global__ void posthoc2_cert_kernel(const uint16_t* __restrict__ pseudo, const double* __restrict__ corr,
-                                     const float* __restrict__ dS, const unsigned long long* __restrict__ red,
-                                     int64_t R, int64_t K, uint64_t sr_head, uint8_t* __restrict__ sf,
-                                     float* __restrict__ scale32_out, uint32_t* __restrict__ listB_n,
-                                     uint32_t* __restrict__ listB, uint32_t* __restrict__ err) {
-  const int64_t gpr = K / GROUP, total = R * gpr;
+// Certified pass 2 (posthoc.py:98-125).  One thread per 4 consecutive groups
+// of a row (one 32-bit store per scale replica).  shifted = pseudo / 2^k is an
+// exact power-of-two multiply; the SR decision lo + (u < p) is taken when the
+// bracket corr * (1 -+ dS) stays inside one E4M3 interval and u is outside the
+// matching p bracket; otherwise the group goes to posthoc_fix2_kernel.
+__device__ __forceinline__ uint32_t sr_certified(double c, double d, double u, bool& ok) {
+  // E4M3 interval [a, b) of c (normal range; smaller values take the exact path)
+  const double lo = c * (1.0 - d), hi = c * (1.0 + d);
+  if (!(lo >= 0x1p-6) || !(hi <= 448.0)) { ok = false; return 0; }
+  const int e = dexp(c);
+  const double step = dpow2(e - 3);                               // b - a, a power of two
+  const double fl = floor(__dmul_rn(c, dpow2(3 - e)));            // 8 + mantissa index
+  const double a = __dmul_rn(fl, step);
+  uint32_t code = ((uint32_t)(e + 7) << 3) + (uint32_t)fl - 8u;
+  if (code > 125u) { ok = false; return 0; }
+  if (!(lo >= a) || !(hi < a + step)) { ok = false; return 0; }  // bracket crosses a grid point
+  const double rs = dpow2(3 - e);
+  const double plo = (lo - a) * rs, phi = (hi - a) * rs;          // p range (monotone in c)
+  if (u < plo) return code + 1;                                    // u < p for every c in the bracket
+  if (u >= phi) return code;
+  ok = false;
+  return 0;
+}
+
+__global__ void __launch_bounds__(256) posthoc2_cert_kernel(
+    const uint16_t* __restrict__ pseudo, const double* __restrict__ corr, const float* __restrict__ dS,
+    const unsigned long long* __restrict__ red, int64_t R, int64_t K, FastDiv fq, uint64_t sr_head,
+    uint8_t* __restrict__ sf, float* __restrict__ scale32_out, uint32_t* __restrict__ listB_n,
+    uint32_t* __restrict__ listB, uint32_t* __restrict__ err) {
+  const uint32_t qpr = (uint32_t)(K / 64), total = (uint32_t)(R * qpr);    // quads of groups per row
   const double pmax = ulong_as_double(red[1]);
-  const float scale32 = posthoc_scale32(pmax);
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g == 0) *scale32_out = scale32;
-  if (g >= total) return;
-  const int64_t r = g / gpr, j = g - r * gpr;
-  const int64_t kpr = kpairs(K);
-  if (pmax == 0.0) { sf_store(sf, r, j, kpr, 0); return; }
-  const double ps = (double)__uint_as_float((uint32_t)pseudo[g] << 16);
-  const double shifted = __ddiv_rn(ps, (double)scale32);
-  const int64_t ch = r * (K / CHUNK) + j / 8;
-  const double S = corr[ch];
-  const double u = prng_uniform(sr_head, (uint64_t)g);
-  const float d = dS[ch];
-  if (d == 0.f) {
-    const double corrected = __dmul_rn(S, shifted);
-    if (corrected > 448.0) atomic_or_err(err, Q2_ERR_SCALE448);
-    sf_store(sf, r, j, kpr, (uint8_t)e4m3_sr(fmin(corrected, 448.0), u));
-    return;
+  int k = 0;
+  if (pmax > 0.0) {
+    int e; const double m = frexp(pmax / 256.0, &e);
+    k = (m == 0.5) ? e - 1 : e;                                             // ms_eden.py:86-91
   }
-  const double cm = __dmul_rn(S, shifted);
-  const double lo = cm * (1.0 - (double)d), hi = cm * (1.0 + (double)d);
-  const uint32_t clo = e4m3_sr(fmin(lo, 448.0), u), chi = e4m3_sr(fmin(hi, 448.0), u);
-  if (clo == chi && hi <= 448.0 && d < 1e-3f) { sf_store(sf, r, j, kpr, (uint8_t)clo); return; }
-  listB[atomicAdd(listB_n, 1u)] = (uint32_t)g;
+  const float scale32 = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
+  const double inv_scale = pmax > 0.0 ? ldexp(1.0, -k) : 0.0;
+  const uint32_t tq = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tq == 0) *scale32_out = scale32;
+  if (tq >= total) return;
+  const uint32_t r = fq.div(tq), jq = tq - r * qpr;                         // groups 4jq .. 4jq+3
+  const int64_t kpr = kpairs(K);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, kpr));
+  if (pmax == 0.0) { dst[0] = 0; dst[256] = 0; dst[512] = 0; dst[768] = 0; return; }
+  const int64_t ch = (int64_t)r * (K / CHUNK) + (jq >> 1);
+  const double S = corr[ch];
+  const double d = (double)dS[ch] * 1.0001;
+  const uint2 pw = *reinterpret_cast<const uint2*>(pseudo + (int64_t)r * (K / GROUP) + 4 * jq);
+  const uint32_t pv[4] = {pw.x & 0xFFFF, pw.x >> 16, pw.y & 0xFFFF, pw.y >> 16};
+  uint32_t word = 0;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t g = (uint64_t)r * (K / GROUP) + 4 * jq + i;
+    const double ps = (double)__uint_as_float(pv[i] << 16);
+    const double corrected = __dmul_rn(S, __dmul_rn(ps, inv_scale));
+    const double u = prng_uniform(sr_head, g);
+    bool ok = d > 0.0;
+    uint32_t code = ok ? sr_certified(corrected, d, u, ok) : 0u;
+    if (!ok) {
+      if (d == 0.0) {                                                       // exact factor (fix-up 1)
+        if (corrected > 448.0) bad = true;
+        code = e4m3_sr(fmin(corrected, 448.0), u);
+      } else {
+        listB[atomicAdd(listB_n, 1u)] = (uint32_t)g;                        // exact re-do
+        code = 0;
+      }
+    }
+    word |= code << (8 * i);
+  }
+  if (bad) atomic_or_err(err, Q2_ERR_SCALE448);
+  dst[0] = word; dst[256] = word; dst[512] = word; dst[768] = word;
 }
 
 // Exact re-do of pass-2 groups (exact float64 EDEN factor of their chunk).
@@ -550,9 +589,10 @@ static int posthoc_fast(MsedArgs a, FastArgs f, uint32_t* listB_n, uint32_t* lis
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   posthoc_fix1_kernel<SRC><<<2 * nsm, 128, 0, st>>>(a, f.dS, f.listA_n, f.listA);
   Q2_CHECK_LAUNCH();
-  const int64_t groups = a.R * (a.K / GROUP);
-  posthoc2_cert_kernel<<<(unsigned)std::max<int64_t>(1, (groups + 255) / 256), 256, 0, st>>>(
-      a.pseudo, a.corr, f.dS, a.red, a.R, a.K, sr_head, a.sf, a.scale32, listB_n, listB, a.err);
+  const int64_t quads = a.R * (a.K / 64);
+  posthoc2_cert_kernel<<<(unsigned)std::max<int64_t>(1, (quads + 255) / 256), 256, 0, st>>>(
+      a.pseudo, a.corr, f.dS, a.red, a.R, a.K, FastDiv((uint32_t)(a.K / 64)), sr_head, a.sf, a.scale32, listB_n,
+      listB, a.err);
   Q2_CHECK_LAUNCH();
   posthoc_fix2_kernel<SRC><<<2 * nsm, 128, 0, st>>>(a, listB_n, listB, sr_head);
   Q2_CHECK_LAUNCH();
