@@ -130,6 +130,18 @@ int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr, const uint
                      int64_t R, int64_t K, uint64_t seed_sr, uint64_t sr_stream,
                      const q2_nvfp4* out, uint32_t* err, void* stream);
 
+/* Both backward operands that read E, from ONE read of E, post-hoc schedule:
+ *  out_rows = pass2(pass1(E))      rows of E along N  (dgrad operand, pair_dx)
+ *  out_cols = pass2(pass1(E^T))    rows of E^T along T (wgrad operand, pair_dw)
+ * (linear_graph.py:306 and :325 with the posthoc.py:74-125 quantizer).  E is
+ * bf16 [T, N] (row stride ld), T % 128 == N % 128 == 0.  The Hadamard rotations
+ * run on the tensor cores (tcgen05 kind::f16 against resident H.diag(signs)).
+ * ws_rows / ws_cols: q2_msed_ws_bytes(T, N) / q2_msed_ws_bytes(N, T).          */
+int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
+                         const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
+                         uint64_t sr_stream_rows, uint64_t sr_stream_cols, const q2_nvfp4* out_rows,
+                         const q2_nvfp4* out_cols, void* ws_rows, void* ws_cols, uint32_t* err, void* stream);
+
 /* NVFP4 "TN" GEMM on tcgen05 block-scaled MMAs (kind::mxf4nvf4, UE4M3 scales
  * per 16, FP32 accumulation in TMEM):  D[M, N] = alpha * A[M,K] . B[N,K]^T
  * with alpha = *a->scale32 * *b->scale32 (+ beta*D if accumulate).

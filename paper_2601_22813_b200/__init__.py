@@ -8,7 +8,8 @@ meanings, computed by hand-written sm_100a CUDA in ``libquartet2.so``.
 from .rht import CHUNK, SeedPair, derive_stream, prng_uniform, sign_mask
 from .quantizers import (GROUP, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
                          quantize_rtn, quantize_rtn_46, set_error_mode)
-from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, pass1, pass2,
+from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
+                      pass1, pass2,
                       posthoc_quantize)
 from .linear_graph import (GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config, forward,
                            gemm, gemm_emulated)
@@ -16,7 +17,7 @@ from .linear_graph import (GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, 
 __all__ = [
     "CHUNK", "GROUP", "GUARDED_SCALE_CAP", "FP8_RTN_MARGIN", "SeedPair", "derive_stream", "prng_uniform",
     "sign_mask", "NVFP4Tensor", "quantize_rtn", "quantize_rtn_46", "dequantize", "check_errors",
-    "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "pass1", "pass2", "posthoc_quantize",
+    "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual_posthoc", "pass1", "pass2", "posthoc_quantize",
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW",
 ]

@@ -23,7 +23,7 @@ Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF = 1, 2, 4, 
 EXPORTS = (
     "q2_sf_bytes", "q2_version", "q2_amax", "q2_quant_fwd_ws_bytes", "q2_quant_fwd",
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
-    "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
+    "q2_msed_dual_posthoc", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
 )
 
 
@@ -52,6 +52,8 @@ _SIGS = {
     "q2_msed_quant": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _U64, _U64, _I, _TP, _P, _P, _P]),
     "q2_posthoc_pass1": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _P, _P, _P, _P, _P, _P]),
     "q2_posthoc_pass2": (_I, [_P, _P, _P, _I64, _I64, _U64, _U64, _TP, _P, _P]),
+    "q2_msed_dual_posthoc": (_I, [_P, _I64, _I64, _I64, _U32x4, _U32x4, _D, _D, _U64, _U64, _U64, _TP, _TP, _P, _P,
+                                  _P, _P]),
     "q2_gemm_tn": (_I, [_TP, _TP, _P, _I, _I64, _I, _P]),
     "q2_dequant": (_I, [_TP, _P, _P]),
     "q2_unpack": (_I, [_TP, _P, _P, _P]),

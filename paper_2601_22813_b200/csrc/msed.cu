@@ -13,7 +13,7 @@
 // (_kernels.py:175-187): every output of every stage is one IEEE add/sub of
 // two stage inputs, so the result does not depend on which lane computes it.
 #include <cuda_fp16.h>
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace q2 {
 
@@ -512,6 +512,7 @@ __global__ void posthoc2_kernel(const uint16_t* __restrict__ pseudo, const doubl
 
 }  // namespace q2
 #include "msed_fast.cuh"
+#include "msed_tc.cuh"
 namespace q2 {
 
 constexpr size_t MSED_SMEM = TILE_ROWS * TILE_LD * sizeof(float) + 8 * 256 * sizeof(double);
@@ -577,13 +578,17 @@ static int launch_fast1(const MsedArgs& a, const FastArgs& f, cudaStream_t st) {
   return Q2_OK;
 }
 
-// Single-read post-hoc MS-EDEN with certified fast paths and exact fix-ups.
+static int num_sms() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+
+// Fix-ups and certified pass 2 after any pass-1 producer.
 template <int SRC>
-static int posthoc_fast(MsedArgs a, FastArgs f, uint32_t* listB_n, uint32_t* listB, uint64_t sr_head,
+static int posthoc_tail(const MsedArgs& a, const FastArgs& f, uint32_t* listB_n, uint32_t* listB, uint64_t sr_head,
                         cudaStream_t st) {
-  int rc = (SRC == Q2_SRC_TAPE_COLS || a.dtype == Q2_BF16) ? launch_fast1<SRC, Q2_BF16>(a, f, st)
-                                                            : launch_fast1<SRC, Q2_F32>(a, f, st);
-  if (rc) return rc;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -597,6 +602,81 @@ static int posthoc_fast(MsedArgs a, FastArgs f, uint32_t* listB_n, uint32_t* lis
   posthoc_fix2_kernel<SRC><<<2 * nsm, 128, 0, st>>>(a, listB_n, listB, sr_head);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
+}
+
+// Single-read post-hoc MS-EDEN with certified fast paths and exact fix-ups.
+template <int SRC>
+static int posthoc_fast(MsedArgs a, FastArgs f, uint32_t* listB_n, uint32_t* listB, uint64_t sr_head,
+                        cudaStream_t st) {
+  int rc = (SRC == Q2_SRC_TAPE_COLS || a.dtype == Q2_BF16) ? launch_fast1<SRC, Q2_BF16>(a, f, st)
+                                                            : launch_fast1<SRC, Q2_F32>(a, f, st);
+  if (rc) return rc;
+  return posthoc_tail<SRC>(a, f, listB_n, listB, sr_head, st);
+}
+
+// Workspace carve-up shared by the post-hoc drivers.
+struct PosthocWs {
+  uint32_t* red; uint16_t* pseudo; double* corr; FastArgs f; uint32_t* listB; uint32_t* listB_n;
+};
+static size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+static PosthocWs carve_ws(void* ws, int64_t R, int64_t K) {
+  PosthocWs w;
+  char* b = static_cast<char*>(ws);
+  const size_t g = (size_t)R * (K / 16), ch = (size_t)R * (K / 128);
+  w.red = reinterpret_cast<uint32_t*>(b);
+  w.pseudo = reinterpret_cast<uint16_t*>(b + 256);
+  w.corr = reinterpret_cast<double*>(b + 256 + al256(g * 2));
+  char* p = b + 256 + al256(g * 2) + al256(ch * 8);
+  w.f.dS = reinterpret_cast<float*>(p);
+  p += al256(ch * 4);
+  w.f.listA = reinterpret_cast<uint32_t*>(p);
+  p += al256(ch * 4);
+  w.listB = reinterpret_cast<uint32_t*>(p);
+  w.f.listA_n = w.red + 4;
+  w.listB_n = w.red + 5;
+  return w;
+}
+
+// Tensor-core pass 1 for bf16 rows / E^T of the same tile; do_rows / do_cols select outputs.
+static int tc_pass1(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t* sign_rows,
+                    const uint32_t* sign_cols, double s, double inv_sqrt, const q2_nvfp4* out_rows,
+                    const q2_nvfp4* out_cols, const PosthocWs* w_rows, const PosthocWs* w_cols, uint32_t* err,
+                    cudaStream_t st) {
+  TcArgs t{};
+  t.do_rows = out_rows != nullptr;
+  t.do_cols = out_cols != nullptr;
+  t.tiles_r = (int)(T / 128);
+  t.tiles_c = (int)(N / 128);
+  t.c_eff = inv_sqrt;
+  t.s = s;
+  t.err = err;
+  for (int j = 0; j < 2; ++j) {
+    const q2_nvfp4* o = j ? out_cols : out_rows;
+    const PosthocWs* w = j ? w_cols : w_rows;
+    const uint32_t* sg = j ? sign_cols : sign_rows;
+    if (!o) continue;
+    t.out[j] = TcOut{o->codes, w->pseudo, w->corr, w->f.dS, reinterpret_cast<unsigned long long*>(w->red),
+                     w->f.listA_n, w->f.listA, j ? N : T, j ? T : N, 0};
+    for (int i = 0; i < 4; ++i) t.sign[j][i] = sg[i];
+  }
+  CUtensorMap mx;
+  if (!make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, x, (uint64_t)N, (uint64_t)T, (uint64_t)ld * 2, 64, 128))
+    return Q2_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(msed_dual_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) != cudaSuccess)
+      return Q2_ECUDA;
+    attr = true;
+  }
+  const int ntiles = t.tiles_r * t.tiles_c;
+  msed_dual_tc_kernel<<<std::min(ntiles, num_sms()), TC_THREADS, TC_SMEM, st>>>(mx, t);
+  Q2_CHECK_LAUNCH();
+  return Q2_OK;
+}
+
+static bool tc_ok(const void* x, int dtype, int64_t T, int64_t N, int64_t ld) {
+  return dtype == Q2_BF16 && T % 128 == 0 && N % 128 == 0 && T > 0 && N > 0 && (ld * 2) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(x) & 15) == 0 && !getenv("Q2_NO_TC_MSED");
 }
 
 }  // namespace q2
@@ -669,6 +749,18 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
     a.codes = out->codes; a.sf = out->sf; a.scale32 = out->scale32;
     a.pseudo = pseudo; a.corr = corr;
     const uint64_t head = prng_head(seed_sr, sr_stream);
+    if (src_kind != Q2_SRC_TAPE_COLS) {
+      const int64_t T = src_kind == Q2_SRC_ROWS ? R : K, N = src_kind == Q2_SRC_ROWS ? K : R;
+      if (tc_ok(x, dtype, T, N, ld)) {
+        const PosthocWs w = carve_ws(ws, R, K);
+        rc = src_kind == Q2_SRC_ROWS
+                 ? tc_pass1(x, T, N, ld, a.sign, a.sign, s, inv_sqrt_chunk, out, nullptr, &w, nullptr, err, st)
+                 : tc_pass1(x, T, N, ld, a.sign, a.sign, s, inv_sqrt_chunk, nullptr, out, nullptr, &w, err, st);
+        if (rc) return rc;
+        return src_kind == Q2_SRC_ROWS ? posthoc_tail<Q2_SRC_ROWS>(a, f, cnt + 1, listB, head, st)
+                                       : posthoc_tail<Q2_SRC_COLS>(a, f, cnt + 1, listB, head, st);
+      }
+    }
     switch (src_kind) {
       case Q2_SRC_ROWS: return posthoc_fast<Q2_SRC_ROWS>(a, f, cnt + 1, listB, head, st);
       case Q2_SRC_COLS: return posthoc_fast<Q2_SRC_COLS>(a, f, cnt + 1, listB, head, st);
@@ -685,4 +777,39 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   rc = a.pow2 ? dispatch_src<PASS_PMAX>(src_kind, a, st) : dispatch_src<PASS_ABSMAX>(src_kind, a, st);
   if (rc) return rc;
   return dispatch_src<PASS_QUANT>(src_kind, a, st);
+}
+
+// Both backward operands that read E in one pass: MS(E) along rows (dgrad, pair
+// sign_rows / sr_stream_rows) and MS(E^T) (wgrad, pair sign_cols /
+// sr_stream_cols), post-hoc schedule.  x is bf16 [T, N], T % 128 == N % 128 == 0.
+extern "C" int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
+                                    const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
+                                    uint64_t sr_stream_rows, uint64_t sr_stream_cols, const q2_nvfp4* out_rows,
+                                    const q2_nvfp4* out_cols, void* ws_rows, void* ws_cols, uint32_t* err,
+                                    void* stream) {
+  if (!x || !out_rows || !out_cols || !ws_rows || !ws_cols || out_rows->R != T || out_rows->K != N ||
+      out_cols->R != N || out_cols->K != T || !tc_ok(x, Q2_BF16, T, N, ld))
+    return Q2_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const PosthocWs wr = carve_ws(ws_rows, T, N), wc = carve_ws(ws_cols, N, T);
+  if (cudaMemsetAsync(wr.red, 0, 32, st) != cudaSuccess || cudaMemsetAsync(wc.red, 0, 32, st) != cudaSuccess)
+    return Q2_ECUDA;
+  int rc = tc_pass1(x, T, N, ld, sign_rows, sign_cols, s, inv_sqrt_chunk, out_rows, out_cols, &wr, &wc, err, st);
+  if (rc) return rc;
+  for (int j = 0; j < 2; ++j) {
+    MsedArgs a;
+    rc = fill_args(a, x, Q2_BF16, nullptr, j ? Q2_SRC_COLS : Q2_SRC_ROWS, j ? N : T, j ? T : N, ld,
+                   j ? sign_cols : sign_rows, s, inv_sqrt_chunk);
+    if (rc) return rc;
+    const q2_nvfp4* o = j ? out_cols : out_rows;
+    const PosthocWs& w = j ? wc : wr;
+    a.red = reinterpret_cast<unsigned long long*>(w.red); a.err = err;
+    a.codes = o->codes; a.sf = o->sf; a.scale32 = o->scale32;
+    a.pseudo = w.pseudo; a.corr = w.corr;
+    const uint64_t head = prng_head(seed_sr, j ? sr_stream_cols : sr_stream_rows);
+    rc = j ? posthoc_tail<Q2_SRC_COLS>(a, w.f, w.listB_n, w.listB, head, st)
+           : posthoc_tail<Q2_SRC_ROWS>(a, w.f, w.listB_n, w.listB, head, st);
+    if (rc) return rc;
+  }
+  return Q2_OK;
 }

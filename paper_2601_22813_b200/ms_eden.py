@@ -85,6 +85,37 @@ def msed(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None, mode: 
     return out
 
 
+def msed_dual_posthoc(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: int, rot_cols: int, s=6.0,
+                      err=None):
+    """(posthoc MS(E), posthoc MS(E^T)) from one read of a bf16 E [T, N] (tensor-core rotations).
+
+    Equals (pass2(pass1(E)), pass2(pass1(E^T))) with the given tensor / rotation ids.
+    """
+    s = _grid_s(s)
+    e2, shape, dt = as_device_matrix(e, "E")
+    T, N = e2.shape
+    if dt != _lib.Q2_BF16 or T % CHUNK or N % CHUNK:
+        raise ValueError("msed_dual_posthoc needs a bfloat16 E with both dims multiples of 128")
+    L = _lib.lib()
+    dev = e2.device
+    qr, qc = NVFP4Tensor.empty((T, N), dev), NVFP4Tensor.empty((N, T), dev)
+    wr = torch.empty(L.q2_msed_ws_bytes(T, N), dtype=torch.uint8, device=dev)
+    wc = torch.empty(L.q2_msed_ws_bytes(N, T), dtype=torch.uint8, device=dev)
+    own = err is None
+    if own:
+        err = _err_word(dev)
+    a, b = qr.c(), qc.c()
+    rc = L.q2_msed_dual_posthoc(e2.data_ptr(), T, N, N, _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_rows))),
+                                _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_cols))), s, INV_SQRT_CHUNK,
+                                int(seeds.sr) & (2**64 - 1), sr_stream(int(id_rows)), sr_stream(int(id_cols)),
+                                ctypes.byref(a), ctypes.byref(b), wr.data_ptr(), wc.data_ptr(), err.data_ptr(),
+                                stream_handle())
+    _lib.check(rc, "msed_dual_posthoc")
+    if own:
+        _finish(err)
+    return qr, qc
+
+
 def ms_eden_quantize(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None,
                      pow2_scale: bool = False) -> NVFP4Tensor:
     """Rotate, RTN with cap 256, EDEN-correct, SR the scales (ms_eden.py:116-153)."""

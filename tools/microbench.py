@@ -61,6 +61,9 @@ def main():
             res[f"msed rows {mode} E"] = {"ms": ms, "GB/s": E.numel() * 2.5625 / ms / 1e6}
             ms = timeit(lambda: q2.msed(E, seeds, 6.0, 1, 2, mode, "cols"))
             res[f"msed cols {mode} E"] = {"ms": ms, "GB/s": E.numel() * 2.5625 / ms / 1e6}
+            if mode == "posthoc":
+                ms = timeit(lambda: q2.msed_dual_posthoc(E, seeds, 1, 2, 3, 4))
+                res["msed dual posthoc E (rows+cols)"] = {"ms": ms, "GB/s": E.numel() * 3.125 / ms / 1e6}
             qw = q2.quantize_rtn_46(W)
             ms = timeit(lambda: q2.msed(qw, seeds, 6.0, 1, 2, mode, "tape"))
             res[f"msed tape {mode} W"] = {"ms": ms, "GB/s": W.numel() * 1.125 / ms / 1e6}

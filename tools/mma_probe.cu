@@ -9,12 +9,15 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 __device__ __forceinline__ uint64_t desc_sf(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 32) | (1ull << 46);
 }
+__device__ __forceinline__ uint64_t desc_sf2(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
 template <int N, bool CP>
 __global__ void probe(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
-  for (int i = threadIdx.x; i < (128 + N) * 128 + 8192; i += blockDim.x) sm[i] = (unsigned char)(i * 7);
+  for (int i = threadIdx.x; i < (128 + N) * 128 + 16384; i += blockDim.x) sm[i] = (unsigned char)(i * 7);
   if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); mbar_fence_init(); }
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
@@ -34,9 +37,9 @@ __global__ void probe(int iters, unsigned long long* out) {
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
     for (int i = 0; i < iters; ++i) {
       if (CP) {
-        for (int kk = 0; kk < 4; ++kk) {
-          asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem + 256 + 4 * kk), "l"(desc_sf(sfs + kk * 512)));
-          asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem + 272 + 4 * kk), "l"(desc_sf(sfs + 2048 + kk * 512)));
+        for (int p = 0; p < 2; ++p) {
+          asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem + 256 + 8 * p), "l"(desc_sf2(sfs + p * 4096)));
+          asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tmem + 272 + 8 * p), "l"(desc_sf2(sfs + 8192 + p * 4096)));
         }
       }
       for (int kk = 0; kk < 4; ++kk)
@@ -54,7 +57,7 @@ __global__ void probe(int iters, unsigned long long* out) {
 }
 template <int N, bool CP> void run(int blocks) {
   unsigned long long* d; cudaMalloc(&d, 8 * blocks);
-  int smem = (128 + N) * 128 + 8192 + 1024;
+  int smem = (128 + N) * 128 + 16384 + 1024;
   cudaFuncSetAttribute(probe<N, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
   probe<N, CP><<<blocks, 128, smem>>>(iters, d);
