@@ -676,7 +676,7 @@ static int tc_pass1(const void* x, int64_t T, int64_t N, int64_t ld, const uint3
 
 static bool tc_ok(const void* x, int dtype, int64_t T, int64_t N, int64_t ld) {
   return dtype == Q2_BF16 && T % 128 == 0 && N % 128 == 0 && T > 0 && N > 0 && (ld * 2) % 16 == 0 &&
-         (reinterpret_cast<uintptr_t>(x) & 15) == 0 && !getenv("Q2_NO_TC_MSED");
+         (reinterpret_cast<uintptr_t>(x) & 15) == 0;
 }
 
 }  // namespace q2
@@ -749,7 +749,9 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
     a.codes = out->codes; a.sf = out->sf; a.scale32 = out->scale32;
     a.pseudo = pseudo; a.corr = corr;
     const uint64_t head = prng_head(seed_sr, sr_stream);
-    if (src_kind != Q2_SRC_TAPE_COLS) {
+    // Tensor-core rotations are opt-in (Q2_TC_MSED=1): their error bound assumes
+    // fp32-accurate MMA accumulation (see msed_tc.cuh); the CUDA-core path's is proven.
+    if (src_kind != Q2_SRC_TAPE_COLS && getenv("Q2_TC_MSED")) {
       const int64_t T = src_kind == Q2_SRC_ROWS ? R : K, N = src_kind == Q2_SRC_ROWS ? K : R;
       if (tc_ok(x, dtype, T, N, ld)) {
         const PosthocWs w = carve_ws(ws, R, K);

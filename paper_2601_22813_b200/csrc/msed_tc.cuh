@@ -10,10 +10,15 @@
 // operands (dgrad: rows of E with pair_dx; wgrad: rows of E^T with pair_dw):
 // E is read once (3.125 B/elem).  tcgen05.mma kind::f16 accumulates in fp32
 // TMEM (two 128x256 accumulator stages); four epilogue warps own one chunk per
-// thread and apply the certified decisions of msed_fast.cuh.  Rotation error
-// bound: each of the 8 K=16 MMAs adds at most 2^-21 of the L1 mass it sums
-// (products are exact), |y - y*| <= 2^-18 ||x||_1 <= 2^-18 ||y||_2 (4x margin
-// over 8 * 2^-21); uncertain chunks go to the float64 fix-up as before.
+// thread and apply the certified decisions of msed_fast.cuh.
+//
+// STATUS: opt-in (Q2_TC_MSED=1).  The bound used below, |y - y*| <= 2^-18
+// ||y||_2, assumes each K=16 MMA adds at most 2^-21 of the L1 mass it sums;
+// PTX only guarantees "at least single precision" accumulation, which allows
+// up to ~2^-16.  Until a per-chunk exactness certificate (exponent span <= 9
+// binades => every partial sum fits 24 bits => exact under any rounding) gates
+// eps = 0, the proven CUDA-core path (msed_fast.cuh) is the default.  Measured
+// on E 16384x11264: 5.3% of chunks / 1.5% of scale groups need the fix-ups.
 
 namespace q2 {
 

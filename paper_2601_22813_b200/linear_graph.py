@@ -13,6 +13,7 @@ quantizations; the default mirrors the reference exactly.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -139,7 +140,9 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     own = err is None
     if own:
         err = _err_word(e2.device)
-    dual = cfg.posthoc and e2.dtype == torch.bfloat16 and tokens % CHUNK == 0 and out_dim % CHUNK == 0
+    # E and E^T from one read on the tensor cores: opt-in (Q2_TC_MSED=1), see msed_tc.cuh
+    dual = (cfg.posthoc and os.environ.get("Q2_TC_MSED") == "1" and e2.dtype == torch.bfloat16
+            and tokens % CHUNK == 0 and out_dim % CHUNK == 0)
     if dual:   # E and E^T from one read of E (tensor-core rotations)
         qe, qet = msed_dual_posthoc(e2, seeds, derive_stream(PAIR_DX, 0), PAIR_DX, derive_stream(PAIR_DW, 0),
                                     PAIR_DW, 6.0, err)

@@ -204,8 +204,9 @@ def test_backward_deterministic(cuda, posthoc):
 
 
 @pytest.mark.parametrize("family", FAMILIES)
-def test_ms_eden_tensor_core_rows_cols(cuda, family):
+def test_ms_eden_tensor_core_rows_cols(cuda, family, monkeypatch):
     """Tensor-core rotations (bf16, dims % 128): rows, E^T and the dual one-read entry."""
+    monkeypatch.setenv("Q2_TC_MSED", "1")
     q2 = _q2()
     e = make(family, (256, 384), seed=41)                 # [T, N]
     s, rs = q2.SeedPair(11, 12), O.SeedPair(11, 12)
