@@ -1,0 +1,664 @@
+// MS-EDEN in literal float64 on the B200 FP64 pipe (included by msed.cu).
+//
+// B200 (sm_100a) executes DADD/DMUL/DFMA at half the FP32 rate (measured 62
+// lanes/clk/SM, tools/f64_probe.cu), so the reference's float64 arithmetic can
+// be restated literally at ~1 Telem/s: every value this kernel produces is the
+// reference's bit for bit by construction, with no certification margins and
+// no fix-up lists.
+//
+//   x_rot  rht.py:144-155 / _kernels.py:175-187: y = FWHT(x * signs) * 128**-0.5,
+//          butterflies h = 1, 2, .., 64 in float64; every output of every stage
+//          is one IEEE add/sub of two stage inputs, so any lane assignment gives
+//          the reference's bits (cross-lane stages use fma(+-1, y, o)).
+//   d      posthoc pass 1 (posthoc.py:83): E8M3_RTN(fl64(gmax / s));
+//          ms_eden_quantize (quantizers.py:177-178): E4M3(s8) * scale32.
+//   codes  _nb_rtn (_kernels.py:101-127): fp32 brackets [q(1-2^-19), q(1+2^-19)]
+//          through cvt.rn.satfinite.e2m1x2 (same ties-to-even rule); an element
+//          whose brackets disagree takes the exact float64 threshold path.
+//   S      chunk_correction_factors (ms_eden.py:75-83): products materialised,
+//          numpy's 8-accumulator pairwise order; the lane layout below makes the
+//          8 accumulators lane-local.
+//   SR     formats.py:174-201 with u = prng_uniform(seed_sr, stream, g).  In
+//          post-hoc mode the scale shift 2^-k (posthoc.py:110-118) is a power of
+//          two, so the E4M3 truncation a and the decision u < p of
+//          v = fl64(S * pseudo) are final in pass 1 whenever the shifted value
+//          is E4M3-normal; pass 2 (q2_msed_pass2_kernel) only re-biases the
+//          exponent, and handles the subnormal RTN branch from (a, v == a).
+//
+// Lane layout: a warp owns 8 rows (128-element chunks); lane = 4*row + q holds
+// elements e = 8k + 2q + b (k = 0..15, b = 0..1) -- exactly the fragment
+// ldmatrix.m8n8 delivers (.trans for E^T / tape sources).  Butterfly bits
+// 0 and 3..6 are lane-local, bits 1..2 cross lanes (shuffles).
+//
+// Persistent CTA: warp 8 is the TMA producer (STAGES-deep ring of 64-row x
+// 128-column tiles), warps 0..7 compute.
+
+namespace q2 {
+
+enum { M64_ABSMAX = 0, M64_PMAX = 1, M64_QUANT = 2, M64_POSTHOC = 3 };
+constexpr int M64_ROWS = 64;                      // logical rows per tile
+constexpr int M64_CONSUMERS = 256;
+constexpr int M64_THREADS = M64_CONSUMERS + 32;
+
+struct M64Args {
+  const uint8_t* tape_sf; const float* tape_scale32;
+  int64_t R, K;                                   // logical tensor [R, K], rotated along K
+  uint32_t sign[4];
+  double s, inv_sqrt;
+  uint64_t sr_head;
+  int pow2;                                       // M64_QUANT: scale32 = 2^k from red[1]
+  uint8_t* codes; uint8_t* sf; float* scale32;
+  uint16_t* aword;                                // posthoc: per-group SR word (see pack_aword)
+  uint16_t* pseudo; double* corr;                 // optional posthoc pass-1 API outputs
+  unsigned long long* red;                        // [0] |x_rot| max, [1] pseudo max (f64 bits)
+  uint32_t* err;
+  int tiles_r, tiles_c;
+};
+
+template <int SRC, int DT>
+struct M64Tile {
+  static constexpr int RAW = SRC == Q2_SRC_TAPE_COLS ? 4096 + 1024 : (DT == Q2_BF16 ? 16384 : 32768);
+  static constexpr int STAGES = SRC == Q2_SRC_TAPE_COLS ? 6 : (DT == Q2_BF16 ? 4 : 3);
+  static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? 2 * 16384 : 0;     // decoded f16 tiles
+  static constexpr int OFF_DEC = STAGES * RAW;
+  static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 8 x 640 B
+  static constexpr int OFF_BAR = OFF_CST + 8 * 640;
+  static constexpr int SMEM = OFF_BAR + 128 + 1024;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ uint64_t dbits(double v) { return (uint64_t)__double_as_longlong(v); }
+__device__ __forceinline__ double bitsd(uint64_t b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// fl64(FP4[code] * d) by exponent arithmetic: |FP4| = 2^((m>>1)-1) * (1 or 1.5),
+// d15 = 1.5 d (exact).  d > 0 normal.
+__device__ __forceinline__ double fp4_times(uint32_t code, double d, double d15) {
+  const uint32_t m = code & 7u;
+  const uint64_t base = dbits((m & 1u) && m > 1u ? d15 : d);
+  const uint64_t v = base + ((uint64_t)(int64_t)((int)(m >> 1) - 1) << 52) + ((uint64_t)(code & 8u) << 60);
+  return m ? bitsd(v) : 0.0;
+}
+// Round a positive normal float to 4 significant bits (E8M3 grid), ties to even.
+__device__ __forceinline__ uint32_t rne4(float g) {
+  const uint32_t b = __float_as_uint(g);
+  return (b + 0x7FFFFu + ((b >> 20) & 1u)) & 0xFFF00000u;
+}
+
+// Exact _nb_rtn code of a float64 value for a positive scale d (threshold form
+// of fl64(v/d) rounding; exact for any float64 v because t*d
+// has <= 7 significant bits).
+__device__ __noinline__ uint32_t rtn_code_exact(double v, double d) {
+  const double a = fabs(v);
+  uint32_t c = 0;
+  c += a > __dmul_rn(0.25, d); c += a >= __dmul_rn(0.75, d); c += a > __dmul_rn(1.25, d);
+  c += a >= __dmul_rn(1.75, d); c += a > __dmul_rn(2.5, d); c += a >= __dmul_rn(3.5, d);
+  c += a > __dmul_rn(5.0, d);
+  return c | (signbit(v) ? 8u : 0u);
+}
+
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+// E2M1 codes (cvt.rn.satfinite, ties to even = _nb_rtn's rule) of 4 packed f32
+// pairs for the lower and upper brackets; byte i = pair i, low nibble = .x.
+__device__ __forceinline__ void codes8(const uint64_t (&lo)[4], const uint64_t (&hi)[4], uint32_t& wlo, uint32_t& whi) {
+  asm("{\n\t.reg .b8 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .f32 x<8>, z<8>;\n\t"
+      "mov.b64 {x0, x1}, %2;\n\tmov.b64 {x2, x3}, %3;\n\tmov.b64 {x4, x5}, %4;\n\tmov.b64 {x6, x7}, %5;\n\t"
+      "mov.b64 {z0, z1}, %6;\n\tmov.b64 {z2, z3}, %7;\n\tmov.b64 {z4, z5}, %8;\n\tmov.b64 {z6, z7}, %9;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 a0, x1, x0;\n\tcvt.rn.satfinite.e2m1x2.f32 a1, x3, x2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 a2, x5, x4;\n\tcvt.rn.satfinite.e2m1x2.f32 a3, x7, x6;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, z1, z0;\n\tcvt.rn.satfinite.e2m1x2.f32 b1, z3, z2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, z5, z4;\n\tcvt.rn.satfinite.e2m1x2.f32 b3, z7, z6;\n\t"
+      "mov.b32 %0, {a0, a1, a2, a3};\n\tmov.b32 %1, {b0, b1, b2, b3};\n\t}"
+      : "=r"(wlo), "=r"(whi)
+      : "l"(lo[0]), "l"(lo[1]), "l"(lo[2]), "l"(lo[3]), "l"(hi[0]), "l"(hi[1]), "l"(hi[2]), "l"(hi[3]));
+}
+
+// Post-hoc SR word of v = fl64(S * pseudo) >= 0: the E4M3-style truncation a
+// (biased binade exponent eb = E + 256, 3 mantissa bits), the SR decision
+// up = u < p with p = (v - a) / ulp exact, and whether v == a.
+//   bits 15..7 eb (0: v == 0), 6..4 m3, 3 up, 2 exact.
+__device__ __forceinline__ uint16_t pack_aword(double v, uint64_t u53) {
+  const uint64_t b = dbits(v);
+  if (b == 0) return 0;
+  int E = (int)((b >> 52) & 0x7FF) - 1023;
+  if (E < -255) return 0;                              // shifted value < 2^-121: code 0
+  if (E > 255) return (uint16_t)(511u << 7);           // certainly > 448 after any shift
+  const uint64_t low49 = b & ((1ull << 49) - 1);
+  const uint32_t m3 = (uint32_t)((b >> 49) & 7);
+  const uint32_t up = u53 < (low49 << 4) ? 1u : 0u;
+  return (uint16_t)(((uint32_t)(E + 256) << 7) | (m3 << 4) | (up << 3) | (low49 == 0 ? 4u : 0u));
+}
+
+// E4M3 code of x = a * 2^-k (+ SR) from an aword; *ovf when x > 448.
+__device__ __forceinline__ uint32_t aword_code(uint32_t w, int k, bool* ovf) {
+  const uint32_t eb = w >> 7;
+  if (eb == 0) return 0;
+  const int E = (int)eb - 256 - k;
+  const uint32_t m3 = (w >> 4) & 7, up = (w >> 3) & 1, exact = (w >> 2) & 1;
+  if (E >= -6) {                                       // E4M3-normal: SR path
+    if (E > 8 || (E == 8 && (m3 == 7 || (m3 == 6 && !exact)))) { *ovf = true; return 126u; }
+    if (E == 8 && m3 == 6) return 126u;                // x == 448
+    return ((uint32_t)(E + 7) << 3) + m3 + up;
+  }
+  // x < 2^-6: RTN on the 2^-9 grid (formats.py:179-181), x*512 = (8+m3) 2^-s
+  const int s = min(-(E + 6), 31);
+  const uint32_t n = 8 + m3;
+  const uint32_t f = s >= 5 ? 0u : (n >> s), rem = s >= 5 ? n : (n & ((1u << s) - 1)), half = 1u << (s - 1);
+  if (s >= 5) return 0;                                // x*512 < 1/2... (n < 16 <= half)
+  if (rem > half) return f + 1;
+  if (rem == half) return exact ? f + (f & 1u) : f + 1;
+  return f;
+}
+
+// E4M3 stochastic rounding of a directly-known corrected scale x (exact /
+// pow2 MS-EDEN, ms_eden.py:142-152): same decomposition without a shift.
+__device__ __forceinline__ uint32_t sr_code_direct(double x, uint64_t u53, bool* ovf) {
+  if (x > 448.0) { *ovf = true; return 126u; }
+  return aword_code(pack_aword(x, u53), 0, ovf);
+}
+
+template <int SRC, int DT, int MODE>
+__global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_constant__ CUtensorMap tm, M64Args a) {
+  using TL = M64Tile<SRC, DT>;
+  extern __shared__ __align__(1024) unsigned char m64_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(m64_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TL::OFF_BAR);
+  const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + TL::STAGES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = a.tiles_r * a.tiles_c;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TL::STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, SRC == Q2_SRC_TAPE_COLS ? M64_CONSUMERS / 32 : 8);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+      const int64_t kp = kpairs(a.R);
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
+        const int s = it % TL::STAGES;
+        if (it >= TL::STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / TL::STAGES) - 1) & 1);
+        const uint32_t dst = smem_u32(smem + s * TL::RAW), fb = bar_full + 8 * s;
+        mbar_expect_tx(fb, TL::RAW);
+        if (SRC == Q2_SRC_ROWS) {
+          const int nb = DT == Q2_BF16 ? 2 : 4, w = DT == Q2_BF16 ? 64 : 32;
+          for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 8192, &tm, tc * CHUNK + j * w, tr * M64_ROWS, fb);
+        } else if (SRC == Q2_SRC_COLS) {
+          const int nb = DT == Q2_BF16 ? 1 : 2;
+          for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 16384, &tm, tr * M64_ROWS + j * 32, tc * CHUNK, fb);
+        } else {
+          tma_load_2d(dst, &tm, tr * 32, tc * CHUNK, fb);                  // codes [128 tape rows x 32 B]
+          bulk_load(dst + 4096, a.tape_sf + (((int64_t)tc * kp + (tr >> 1)) << 12), 1024, fb);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int q = lane & 3, rw = lane >> 2;
+  uint32_t sg[16];                                  // sign XOR words per block k (bf16 / f32 sources)
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int e = 8 * k + 2 * q;
+    const uint32_t s0 = (a.sign[e >> 5] >> (e & 31)) & 1u, s1 = (a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u;
+    sg[k] = DT == Q2_BF16 && SRC != Q2_SRC_TAPE_COLS ? (s0 << 15) | (s1 << 31) : (s0 | (s1 << 1));
+  }
+  const double tape_s = SRC == Q2_SRC_TAPE_COLS ? (double)__ldg(a.tape_scale32) : 1.0;
+  float scale32 = 0.f;
+  bool zero = false;                                 // all-zero tensor (quantizers.py:175-176)
+  double sdiv = a.s;                                 // gmax / sdiv -> scale candidate
+  if (MODE == M64_QUANT) {
+    const double amax = bitsd(a.red[0]);
+    zero = amax == 0.0;
+    if (zero) scale32 = 0.f;
+    else if (a.pow2) {
+      const double pmax = bitsd(a.red[1]);
+      int k2 = 0;
+      if (pmax > 0.0) { int e; const double m = frexp(pmax / 256.0, &e); k2 = (m == 0.5) ? e - 1 : e; }
+      scale32 = (float)ldexp(1.0, k2);
+    } else {
+      scale32 = __double2float_rn(__ddiv_rn(amax, __dmul_rn(a.s, 256.0)));
+    }
+    sdiv = __dmul_rn((double)scale32, a.s);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.scale32 = scale32;
+  }
+  // directed-rounding fp32 reciprocals bracketing 1/s and 1/(scale32 s)
+  const float is_lo = __frcp_rd(__double2float_ru(a.s)), is_hi = __frcp_ru(__double2float_rd(a.s));
+  const float isd_lo = __frcp_rd(__double2float_ru(sdiv)), isd_hi = __frcp_ru(__double2float_rd(sdiv));
+  const int64_t gpr = a.K / GROUP;
+  uint64_t wabs = 0, wp = 0;                          // running |y| max / pseudo max (f64 bits)
+  bool bad = false, ovf = false, nanscale = false;
+
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
+    const int s = it % TL::STAGES;
+    mbar_wait_sleep(bar_full + 8 * s, (it / TL::STAGES) & 1);
+    const uint32_t st = smem_u32(smem + s * TL::RAW);
+    const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
+    double y[16][2];
+
+    if (SRC == Q2_SRC_TAPE_COLS) {
+      // decode the NVFP4 tape block [128 tape rows x 64 tape cols] into f16 (exact:
+      // FP4*E4M3 has <= 6 significant bits), random sign of the tape row applied
+      unsigned char* dec = smem + TL::OFF_DEC + (it & 1) * 16384;
+      {
+        const int tri = threadIdx.x & 127, h = threadIdx.x >> 7;
+        const uint4 cw = *reinterpret_cast<const uint4*>(smem + s * TL::RAW + tri * 32 + h * 16);
+        const int L = tri & 31;
+        const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + s * TL::RAW + 4096 + ((L >> 3) << 8) +
+                                                                ((tr & 1) << 7) + ((L & 7) << 4) + ((tri >> 5) << 2));
+        const uint32_t neg = ((a.sign[tri >> 5] >> (tri & 31)) & 1u) ? 0x80008000u : 0u;
+        uint32_t sc[2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const uint32_t s8 = (sfw >> (8 * (2 * h + g))) & 0xFF;
+          asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(sc[g]) : "h"((unsigned short)(s8 | (s8 << 8))));
+        }
+        const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
+        uint32_t o[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          uint32_t hv;
+          asm("{\n\t.reg .b8 t;\n\tcvt.u8.u32 t, %1;\n\tcvt.rn.f16x2.e2m1x2 %0, t;\n\t}" : "=r"(hv) : "r"(ww[i >> 2] >> (8 * (i & 3))));
+          // fma with +0 turns the -0 of code 8 into +0, as FP4_VALUES[8] = 0.0
+          asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(o[i]) : "r"(hv), "r"(sc[i >> 3]), "r"(0u));
+          o[i] ^= neg;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          *reinterpret_cast<uint4*>(dec + tri * 128 + (((4 * h + j) ^ (tri & 7)) << 4)) =
+              make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+      named_bar(1, M64_CONSUMERS);
+      const uint32_t db = smem_u32(dec);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t v[4];
+        const int k = 4 * i + (lane >> 3), ri = lane & 7;
+        ldsm_x4_t(db + (8 * k + ri) * 128 + ((warp ^ ri) << 4), v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float f0, f1;
+          asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+              : "=f"(f0), "=f"(f1) : "r"(v[j]));
+          y[4 * i + j][0] = __dmul_rn((double)f0, tape_s);
+          y[4 * i + j][1] = __dmul_rn((double)f1, tape_s);
+        }
+      }
+    } else if (DT == Q2_BF16) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t v[4];
+        const int k = 4 * i + (lane >> 3), ri = lane & 7;
+        if (SRC == Q2_SRC_ROWS)
+          ldsm_x4(st + (k >> 3) * 8192 + (8 * warp + ri) * 128 + (((k & 7) ^ ri) << 4), v);
+        else
+          ldsm_x4_t(st + (8 * k + ri) * 128 + ((warp ^ ri) << 4), v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t w = v[j] ^ sg[4 * i + j];
+          y[4 * i + j][0] = (double)__uint_as_float(w << 16);
+          y[4 * i + j][1] = (double)__uint_as_float(w & 0xFFFF0000u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+    } else {
+      const unsigned char* tile = smem + s * TL::RAW;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int e = 8 * k + 2 * q + b;
+          float f;
+          if (SRC == Q2_SRC_ROWS) {
+            const int row = 8 * warp + rw;
+            f = *reinterpret_cast<const float*>(tile + (e >> 5) * 8192 + row * 128 + ((((e & 31) >> 2) ^ (row & 7)) << 4) + (e & 3) * 4);
+          } else {
+            const int col = 8 * warp + rw;
+            f = *reinterpret_cast<const float*>(tile + (col >> 5) * 16384 + e * 128 + ((((col & 31) >> 2) ^ (e & 7)) << 4) + (col & 3) * 4);
+          }
+          const double v = (double)f;
+          y[k][b] = ((sg[k] >> b) & 1u) ? -v : v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
+    }
+
+    // ---------------------------------------------------------------- FWHT
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {                   // h = 1 (bit b)
+      const double u = y[k][0], v = y[k][1];
+      y[k][0] = __dadd_rn(u, v);
+      y[k][1] = __dsub_rn(u, v);
+    }
+#pragma unroll
+    for (int m = 1; m <= 2; m <<= 1) {               // h = 2, 4 (lane bits of q)
+      const double sgn = (q & m) ? -1.0 : 1.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const double o = __shfl_xor_sync(0xFFFFFFFFu, y[k][b], m);
+          y[k][b] = __fma_rn(sgn, y[k][b], o);        // top: o + y, bottom: o - y (one rounding)
+        }
+    }
+#pragma unroll
+    for (int hk = 1; hk < 16; hk <<= 1)              // h = 8 .. 64 (bits of k)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k & hk) continue;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const double u = y[k][b], v = y[k + hk][b];
+          y[k][b] = __dadd_rn(u, v);
+          y[k + hk][b] = __dsub_rn(u, v);
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      y[k][0] = __dmul_rn(y[k][0], a.inv_sqrt);
+      y[k][1] = __dmul_rn(y[k][1], a.inv_sqrt);
+    }
+
+    // ------------------------------------------------------- group maxima
+    // fp32 truncations rz(y) feed the codes and the group maxima: max |rz(y)| =
+    // rz(max |y|) (rz is monotone), so gmax lies in [gmf, nextup(gmf)).
+    const bool live = r < a.R;
+    float yf[16][2];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { yf[k][0] = __double2float_rz(y[k][0]); yf[k][1] = __double2float_rz(y[k][1]); }
+    if (MODE == M64_ABSMAX || MODE == M64_PMAX || (MODE == M64_POSTHOC && a.pseudo)) {
+      // exact |x_rot| max (exact-mode scale32 / pass-1 API reduction)
+      uint64_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        m = umax64(m, umax64(dbits(y[k][0]) & 0x7FFFFFFFFFFFFFFFull, dbits(y[k][1]) & 0x7FFFFFFFFFFFFFFFull));
+      if (live) wabs = umax64(wabs, m);
+      if (MODE == M64_ABSMAX) continue;
+    }
+    float gv[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      gv[g] = fmaxf(fmaxf(fabsf(yf[2 * g][0]), fabsf(yf[2 * g][1])), fmaxf(fabsf(yf[2 * g + 1][0]), fabsf(yf[2 * g + 1][1])));
+    // reduce-scatter over the quad: lane q ends with groups 2q, 2q+1
+    float w4[4], gq[2];
+    {
+      const bool hi2 = q & 2, hi1 = q & 1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float snd = hi2 ? gv[i] : gv[4 + i], keep = hi2 ? gv[4 + i] : gv[i];
+        w4[i] = fmaxf(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 2));
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float snd = hi1 ? w4[i] : w4[2 + i], keep = hi1 ? w4[2 + i] : w4[i];
+        gq[i] = fmaxf(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 1));
+      }
+    }
+    // ------------------------------------------------------ group scales d
+    // certified from the bracket [gmf, nextup(gmf)) with directed fp32 rounding;
+    // a warp with any uncertain group recomputes its scales from exact maxima.
+    uint32_t dkey[2];                                 // posthoc: d as fp32 bits; quant: s8
+    bool unc = false;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float glo = gq[j], gup = __uint_as_float(__float_as_uint(gq[j]) + 1u);
+      if (MODE == M64_QUANT) {
+        const float lo = __fmul_rd(glo, isd_lo), hi = __fmul_ru(gup, isd_hi);
+        uint32_t cl, ch;
+        asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
+            "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
+            : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(lo), "f"(hi));
+        dkey[j] = zero ? 0u : cl;
+        unc |= !zero && (cl != ch || !(hi < 0x1p120f));
+      } else {
+        const float lo = __fmul_rd(glo, is_lo), hi = __fmul_ru(gup, is_hi);
+        const uint32_t pl = rne4(lo), ph = rne4(hi);
+        dkey[j] = pl;
+        unc |= pl != ph || !(lo >= 0x1p-125f) || !(hi < 0x1p126f);
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, unc)) {
+      uint64_t gm[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const uint64_t M = 0x7FFFFFFFFFFFFFFFull;
+        uint64_t m = umax64(umax64(dbits(y[2 * g][0]) & M, dbits(y[2 * g][1]) & M),
+                            umax64(dbits(y[2 * g + 1][0]) & M, dbits(y[2 * g + 1][1]) & M));
+        m = umax64(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+        gm[g] = umax64(m, __shfl_xor_sync(0xFFFFFFFFu, m, 2));
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint64_t gmq = gm[0];
+#pragma unroll
+        for (int g = 1; g < 8; ++g) gmq = (g == 2 * q + j) ? gm[g] : gmq;
+        const double gmax = bitsd(gmq);
+        if (MODE == M64_QUANT) {
+          double xq = zero ? 0.0 : __ddiv_rn(gmax, sdiv);
+          if (isnan(xq)) { if (live) nanscale = true; xq = 0.0; }
+          dkey[j] = e4m3_rtn(xq);
+        } else {
+          bool o2 = false;
+          const double p = e8m3_rtn(__ddiv_rn(gmax, a.s), &o2);
+          if (live && o2) ovf = true;
+          dkey[j] = __float_as_uint((float)p);
+        }
+      }
+    }
+    if (MODE == M64_PMAX) {
+      if (live) wp = umax64(wp, dbits((double)__uint_as_float(max(dkey[0], dkey[1]))));
+      continue;
+    }
+    // all-gather the 8 group keys of the chunk
+    uint32_t key[8];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) key[2 * p + j] = __shfl_sync(0xFFFFFFFFu, dkey[j], (lane & ~3) | p);
+    double d[8], d15[8];
+    float df[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (MODE == M64_QUANT) {
+        d[g] = __dmul_rn(e4m3_val(key[g]), (double)scale32);
+        d15[g] = __dmul_rn(d[g], 1.5);
+        df[g] = (float)d[g];
+      } else {
+        df[g] = __uint_as_float(key[g]);
+        d[g] = (double)df[g];
+        d15[g] = (double)(df[g] * 1.5f);               // 5 significant bits: exact
+      }
+    }
+
+    // --------------------------------------------------------------- codes
+    // four packed code bytes per word: cw[j] holds blocks 4j..4j+3 (low nibble = even element)
+    uint32_t cw[4];
+    uint32_t diff = 0;
+    bool slow = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint64_t lo2[4], hi2[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = 4 * j + i, g = k >> 1;
+        float inv;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(df[g]));
+        const float ilo = inv * (1.f - 0x1p-19f), ihi = inv * (1.f + 0x1p-19f);
+        const uint64_t y2 = f2pack(yf[k][0], yf[k][1]);
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(lo2[i]) : "l"(y2), "l"(f2pack(ilo, ilo)));
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(hi2[i]) : "l"(y2), "l"(f2pack(ihi, ihi)));
+      }
+      uint32_t wl, wh;
+      codes8(lo2, hi2, wl, wh);
+      cw[j] = wl;
+      diff |= wl ^ wh;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int g = 2 * j + i;
+        slow |= !(df[g] >= 0x1p-125f && df[g] < 0x1p125f);
+      }
+    }
+    if (diff || slow) {                               // exact threshold path (rare, no shuffles)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = 4 * j + i, g = k >> 1;
+          uint32_t c = (cw[j] >> (8 * i)) & 0xFF;
+          const bool bad_pair = ((diff >> (8 * i)) & 0xFF) != 0;
+          if (!(d[g] > 0.0)) c = 0;
+          else if (bad_pair || !(df[g] >= 0x1p-125f && df[g] < 0x1p125f))
+            c = rtn_code_exact(y[k][0], d[g]) | (rtn_code_exact(y[k][1], d[g]) << 4);
+          w |= c << (8 * i);
+        }
+        cw[j] = w;
+      }
+    }
+    // ------------------------------------------------ EDEN factor (numpy order)
+    // x_rtn = FP4[code] * d exactly (posthoc: fp32 product of <= 6 significant bits)
+    double an[2], ad[2];
+    auto eden = [&](auto dqfn) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t cbk = (cw[k >> 2] >> (8 * (k & 3))) & 0xFF;
+        double dq0, dq1;
+        dqfn(k, cbk, dq0, dq1);
+        const double pn0 = __dmul_rn(y[k][0], y[k][0]), pn1 = __dmul_rn(y[k][1], y[k][1]);
+        const double pd0 = __dmul_rn(y[k][0], dq0), pd1 = __dmul_rn(y[k][1], dq1);
+        if (k == 0) { an[0] = pn0; an[1] = pn1; ad[0] = pd0; ad[1] = pd1; }
+        else { an[0] = __dadd_rn(an[0], pn0); an[1] = __dadd_rn(an[1], pn1); ad[0] = __dadd_rn(ad[0], pd0); ad[1] = __dadd_rn(ad[1], pd1); }
+      }
+    };
+    if (MODE == M64_POSTHOC && !slow) {
+      eden([&](int k, uint32_t cbk, double& dq0, double& dq1) {
+        uint32_t h2;
+        asm("{\n\t.reg .b8 t;\n\tcvt.u8.u32 t, %1;\n\tcvt.rn.f16x2.e2m1x2 %0, t;\n\t}" : "=r"(h2) : "r"(cbk));
+        float f0, f1;
+        asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+            : "=f"(f0), "=f"(f1) : "r"(h2));
+        dq0 = (double)(f0 * df[k >> 1]);
+        dq1 = (double)(f1 * df[k >> 1]);
+      });
+    } else {
+      eden([&](int k, uint32_t cbk, double& dq0, double& dq1) {
+        dq0 = fp4_times(cbk & 0xF, d[k >> 1], d15[k >> 1]);
+        dq1 = fp4_times(cbk >> 4, d[k >> 1], d15[k >> 1]);
+      });
+    }
+    double num = __dadd_rn(an[0], an[1]), den = __dadd_rn(ad[0], ad[1]);
+    num = __dadd_rn(num, __shfl_xor_sync(0xFFFFFFFFu, num, 1));
+    den = __dadd_rn(den, __shfl_xor_sync(0xFFFFFFFFu, den, 1));
+    num = __dadd_rn(num, __shfl_xor_sync(0xFFFFFFFFu, num, 2));
+    den = __dadd_rn(den, __shfl_xor_sync(0xFFFFFFFFu, den, 2));
+    if (live && !(num < INFINITY)) bad = true;        // any non-finite input poisons every rotated value
+    const bool okS = (fabs(den) >= __dmul_rn(1e-30, num)) && (num > 0.0);
+    const double S = okS ? __ddiv_rn(num, den) : 1.0;
+
+    // ----------------------------------------------------------- outputs
+    // codes: byte k of this lane is chunk byte 4k + q; stage through smem (80 B row pitch)
+    unsigned char* cst = smem + TL::OFF_CST + warp * 640;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cst[rw * 80 + 4 * k + q] = (unsigned char)(cw[k >> 2] >> (8 * (k & 3)));
+    __syncwarp();
+    const uint4 cw4 = *reinterpret_cast<const uint4*>(cst + rw * 80 + 16 * q);
+    __syncwarp();
+    // per-group scale outputs: lane q owns groups 2q, 2q+1
+    const int64_t g0 = r * gpr + (int64_t)tc * 8 + 2 * q;
+    uint32_t wv[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t z = mix64(a.sr_head ^ ((uint64_t)(g0 + j) + GOLDEN));
+      const double dj = MODE == M64_QUANT ? e4m3_val(dkey[j]) : (double)__uint_as_float(dkey[j]);
+      if (MODE == M64_POSTHOC) {
+        wv[j] = pack_aword(__dmul_rn(S, dj), z >> 11);
+      } else {
+        bool o2 = false;
+        wv[j] = zero ? 0u : sr_code_direct(__dmul_rn(S, dj), z >> 11, &o2);
+        if (live && o2) ovf = true;
+      }
+    }
+    const uint32_t half = wv[0] | (wv[1] << 8);
+    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, half, 1);
+    if (live) {
+      *reinterpret_cast<uint4*>(a.codes + r * (a.K / 2) + (int64_t)tc * 64 + 16 * q) = cw4;
+      if (MODE == M64_POSTHOC) {
+        wp = umax64(wp, dbits((double)__uint_as_float(max(dkey[0], dkey[1]))));
+        if (a.aword) *reinterpret_cast<uint32_t*>(a.aword + g0) = wv[0] | (wv[1] << 16);
+        if (a.pseudo) *reinterpret_cast<uint32_t*>(a.pseudo + g0) = (dkey[0] >> 16) | (dkey[1] & 0xFFFF0000u);
+        if (a.corr && q == 0) a.corr[r * (a.K / CHUNK) + tc] = S;
+      } else if ((q & 1) == 0) {                      // lanes 2m: the 4-scale word of groups 4m..4m+3
+        const uint32_t word = half | (other << 16);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(a.sf + sf_offset(r, (int64_t)tc * 8 + 2 * q, kpairs(a.K)));
+        dst[0] = word; dst[256] = word; dst[512] = word; dst[768] = word;
+      }
+    }
+  }
+
+  // ------------------------------------------------------------- reductions
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wabs = umax64(wabs, __shfl_xor_sync(0xFFFFFFFFu, wabs, o));
+    wp = umax64(wp, __shfl_xor_sync(0xFFFFFFFFu, wp, o));
+  }
+  if (lane == 0) {
+    if (MODE != M64_QUANT && wabs) atomicMax(&a.red[0], (unsigned long long)wabs);
+    if ((MODE == M64_PMAX || MODE == M64_POSTHOC) && wp) atomicMax(&a.red[1], (unsigned long long)wp);
+  }
+  if (bad) atomic_or_err(a.err, Q2_ERR_NONFINITE);
+  if (ovf) atomic_or_err(a.err, MODE == M64_QUANT ? Q2_ERR_SCALE448 : Q2_ERR_E8M3_OVF);
+  if (nanscale) atomic_or_err(a.err, Q2_ERR_NAN_SCALE);
+}
+
+// Post-hoc pass 2 (posthoc.py:98-125): k from the pseudo-scale max, then each
+// group's E4M3 code from its pass-1 SR word.  One thread per 4 groups.
+__global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __restrict__ aword,
+                                                           const unsigned long long* __restrict__ red, int64_t R,
+                                                           int64_t K, uint8_t* __restrict__ sf,
+                                                           float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
+  const int64_t qpr = K / 64, total = R * qpr;
+  const double pmax = __longlong_as_double((long long)red[1]);
+  int k = 0;
+  if (pmax > 0.0) { int e; const double m = frexp(pmax / 256.0, &e); k = (m == 0.5) ? e - 1 : e; }
+  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tq == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
+  if (tq >= total) return;
+  const int64_t r = tq / qpr, jq = tq - r * qpr;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, kpairs(K)));
+  uint32_t word = 0;
+  bool ovf = false;
+  if (pmax > 0.0) {
+    const uint2 w = *reinterpret_cast<const uint2*>(aword + r * (K / GROUP) + 4 * jq);
+    word = aword_code(w.x & 0xFFFF, k, &ovf) | (aword_code(w.x >> 16, k, &ovf) << 8) |
+           (aword_code(w.y & 0xFFFF, k, &ovf) << 16) | (aword_code(w.y >> 16, k, &ovf) << 24);
+  }
+  if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
+  dst[0] = word; dst[256] = word; dst[512] = word; dst[768] = word;
+}
+
+}  // namespace q2

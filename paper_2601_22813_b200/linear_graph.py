@@ -13,13 +13,12 @@ quantizations; the default mirrors the reference exactly.
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import torch
 
 from . import _lib
-from .ms_eden import msed, msed_dual_posthoc
+from .ms_eden import msed
 from .quantizers import NVFP4Tensor, _err_word, _finish, as_device_matrix, quantize_rtn_46, stream_handle
 from .rht import CHUNK, SeedPair, derive_stream
 
@@ -140,20 +139,12 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     own = err is None
     if own:
         err = _err_word(e2.device)
-    # E and E^T from one read on the tensor cores: opt-in (Q2_TC_MSED=1), see msed_tc.cuh
-    dual = (cfg.posthoc and os.environ.get("Q2_TC_MSED") == "1" and e2.dtype == torch.bfloat16
-            and tokens % CHUNK == 0 and out_dim % CHUNK == 0)
-    if dual:   # E and E^T from one read of E (tensor-core rotations)
-        qe, qet = msed_dual_posthoc(e2, seeds, derive_stream(PAIR_DX, 0), PAIR_DX, derive_stream(PAIR_DW, 0),
-                                    PAIR_DW, 6.0, err)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
-    if not dual:
-        qe = msed(e2, seeds, 6.0, derive_stream(PAIR_DX, 0), PAIR_DX, mode, "rows", err)
+    qe = msed(e2, seeds, 6.0, derive_stream(PAIR_DX, 0), PAIR_DX, mode, "rows", err)
     qwt = msed(tape.qW, seeds, 6.0, derive_stream(PAIR_DX, 1), PAIR_DX, mode, "tape", err)
     dx = gemm(qe, qwt, dx_dtype)
     # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens
-    if not dual:
-        qet = msed(e2, seeds, 6.0, derive_stream(PAIR_DW, 0), PAIR_DW, mode, "cols", err)
+    qet = msed(e2, seeds, 6.0, derive_stream(PAIR_DW, 0), PAIR_DW, mode, "cols", err)
     qxt = msed(tape.qX, seeds, 6.0, derive_stream(PAIR_DW, 1), PAIR_DW, mode, "tape", err)
     dw = gemm(qet, qxt, torch.float32)
     if own:

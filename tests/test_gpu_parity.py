@@ -204,15 +204,14 @@ def test_backward_deterministic(cuda, posthoc):
 
 
 @pytest.mark.parametrize("family", FAMILIES)
-def test_ms_eden_tensor_core_rows_cols(cuda, family, monkeypatch):
-    """Tensor-core rotations (bf16, dims % 128): rows, E^T and the dual one-read entry."""
-    monkeypatch.setenv("Q2_TC_MSED", "1")
+def test_ms_eden_rows_cols_dual(cuda, family):
+    """Post-hoc MS(E) and MS(E^T) of one bf16 E (dims % 128), singly and through the dual entry."""
     q2 = _q2()
     e = make(family, (256, 384), seed=41)                 # [T, N]
     s, rs = q2.SeedPair(11, 12), O.SeedPair(11, 12)
-    assert_same(q2.msed(_dev(e), s, 6.0, 3, 4, "posthoc", "rows"), O.posthoc_quantize(e, rs, 6.0, 3, 4), "tc rows")
+    assert_same(q2.msed(_dev(e), s, 6.0, 3, 4, "posthoc", "rows"), O.posthoc_quantize(e, rs, 6.0, 3, 4), "rows")
     et = np.ascontiguousarray(e.T)
-    assert_same(q2.msed(_dev(e), s, 6.0, 5, 6, "posthoc", "cols"), O.posthoc_quantize(et, rs, 6.0, 5, 6), "tc cols")
+    assert_same(q2.msed(_dev(e), s, 6.0, 5, 6, "posthoc", "cols"), O.posthoc_quantize(et, rs, 6.0, 5, 6), "cols")
     qr, qc = q2.msed_dual_posthoc(_dev(e), s, 3, 4, 5, 6)
     assert_same(qr, O.posthoc_quantize(e, rs, 6.0, 3, 4), "dual rows")
     assert_same(qc, O.posthoc_quantize(et, rs, 6.0, 5, 6), "dual cols")

@@ -67,6 +67,9 @@ def main():
             qw = q2.quantize_rtn_46(W)
             ms = timeit(lambda: q2.msed(qw, seeds, 6.0, 1, 2, mode, "tape"))
             res[f"msed tape {mode} W"] = {"ms": ms, "GB/s": W.numel() * 1.125 / ms / 1e6}
+            qx = q2.quantize_rtn_46(X)
+            ms = timeit(lambda: q2.msed(qx, seeds, 6.0, 1, 2, mode, "tape"))
+            res[f"msed tape {mode} X"] = {"ms": ms, "GB/s": X.numel() * 1.125 / ms / 1e6}
     if "gemm" in only:
         for name, (m, n, k) in (("fprop upgate", (T, 11264, 2048)), ("dgrad upgate", (T, 2048, 11264)),
                                 ("wgrad upgate", (11264, 2048, T)), ("fprop o", (T, 2048, 2048)),
