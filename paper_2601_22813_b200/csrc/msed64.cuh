@@ -62,7 +62,8 @@ struct M64Tile {
   static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? 2 * 16384 : 0;     // decoded f16 tiles
   static constexpr int OFF_DEC = STAGES * RAW;
   static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 8 x 640 B
-  static constexpr int OFF_BAR = OFF_CST + 8 * 640;
+  static constexpr int OFF_SGN = OFF_CST + 8 * 640;                      // 4 x 16 sign words
+  static constexpr int OFF_BAR = OFF_SGN + 256;
   static constexpr int SMEM = OFF_BAR + 128 + 1024;
 };
 
@@ -184,6 +185,12 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
     mbar_fence_init();
   }
+  if (threadIdx.x < 64) {
+    const int qq = threadIdx.x >> 4, k = threadIdx.x & 15, e = 8 * k + 2 * qq;
+    const uint32_t s0 = (a.sign[e >> 5] >> (e & 31)) & 1u, s1 = (a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u;
+    reinterpret_cast<uint32_t*>(smem + TL::OFF_SGN)[threadIdx.x] =
+        DT == Q2_BF16 && SRC != Q2_SRC_TAPE_COLS ? (s0 << 15) | (s1 << 31) : (s0 | (s1 << 1));
+  }
   __syncthreads();
 
   if (warp == 8) {
@@ -215,13 +222,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
 
   // -------------------------------------------------------------- consumers
   const int q = lane & 3, rw = lane >> 2;
-  uint32_t sg[16];                                  // sign XOR words per block k (bf16 / f32 sources)
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int e = 8 * k + 2 * q;
-    const uint32_t s0 = (a.sign[e >> 5] >> (e & 31)) & 1u, s1 = (a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u;
-    sg[k] = DT == Q2_BF16 && SRC != Q2_SRC_TAPE_COLS ? (s0 << 15) | (s1 << 31) : (s0 | (s1 << 1));
-  }
+  // sign XOR words per (q, block k) live in smem (bf16: bits 15/31; fp32: bits 0/1)
+  const uint32_t* sgt = reinterpret_cast<const uint32_t*>(smem + TL::OFF_SGN) + 16 * q;
   const double tape_s = SRC == Q2_SRC_TAPE_COLS ? (double)__ldg(a.tape_scale32) : 1.0;
   float scale32 = 0.f;
   bool zero = false;                                 // all-zero tensor (quantizers.py:175-176)
@@ -245,6 +247,9 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   const float is_lo = __frcp_rd(__double2float_ru(a.s)), is_hi = __frcp_ru(__double2float_rd(a.s));
   const float isd_lo = __frcp_rd(__double2float_ru(sdiv)), isd_hi = __frcp_ru(__double2float_rd(sdiv));
   const int64_t gpr = a.K / GROUP;
+  constexpr bool SCALED = DT == Q2_BF16 && SRC != Q2_SRC_TAPE_COLS;     // inputs carried as x * 2^-896
+  const double c_eff = SCALED ? __dmul_rn(a.inv_sqrt, 0x1p896) : a.inv_sqrt;
+  uint32_t m16 = 0;                                  // bf16 |x| bits max (non-finite check)
   uint64_t wabs = 0, wp = 0;                          // running |y| max / pseudo max (f64 bits)
   bool bad = false, ovf = false, nanscale = false;
 
@@ -318,9 +323,14 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           ldsm_x4_t(st + (8 * k + ri) * 128 + ((warp ^ ri) << 4), v);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t w = v[j] ^ sg[4 * i + j];
-          y[4 * i + j][0] = (double)__uint_as_float(w << 16);
-          y[4 * i + j][1] = (double)__uint_as_float(w & 0xFFFF0000u);
+          // bf16 -> float64 * 2^-896 by moving the fields (exact, zeros and subnormals
+          // included); 2^896 is folded into the final 128**-0.5 multiply
+          const uint32_t w = v[j] ^ sgt[4 * i + j];
+          asm("max.u16x2 %0, %0, %1;" : "+r"(m16) : "r"(w & 0x7FFF7FFFu));
+          const uint32_t h0 = ((w << 16) & 0x80000000u) | ((w << 13) & 0x0FFFE000u);
+          const uint32_t h1 = (w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u);
+          y[4 * i + j][0] = bitsd((uint64_t)h0 << 32);
+          y[4 * i + j][1] = bitsd((uint64_t)h1 << 32);
         }
       }
       __syncwarp();
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
             f = *reinterpret_cast<const float*>(tile + (col >> 5) * 16384 + e * 128 + ((((col & 31) >> 2) ^ (e & 7)) << 4) + (col & 3) * 4);
           }
           const double v = (double)f;
-          y[k][b] = ((sg[k] >> b) & 1u) ? -v : v;
+          y[k][b] = ((sgt[k] >> b) & 1u) ? -v : v;
         }
       }
       __syncwarp();
@@ -380,8 +390,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      y[k][0] = __dmul_rn(y[k][0], a.inv_sqrt);
-      y[k][1] = __dmul_rn(y[k][1], a.inv_sqrt);
+      y[k][0] = __dmul_rn(y[k][0], c_eff);
+      y[k][1] = __dmul_rn(y[k][1], c_eff);
     }
 
     // ------------------------------------------------------- group maxima
@@ -391,6 +401,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     float yf[16][2];
 #pragma unroll
     for (int k = 0; k < 16; ++k) { yf[k][0] = __double2float_rz(y[k][0]); yf[k][1] = __double2float_rz(y[k][1]); }
+#define YF(k, b) yf[k][b]
     if (MODE == M64_ABSMAX || MODE == M64_PMAX || (MODE == M64_POSTHOC && a.pseudo)) {
       // exact |x_rot| max (exact-mode scale32 / pass-1 API reduction)
       uint64_t m = 0;
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     float gv[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g)
-      gv[g] = fmaxf(fmaxf(fabsf(yf[2 * g][0]), fabsf(yf[2 * g][1])), fmaxf(fabsf(yf[2 * g + 1][0]), fabsf(yf[2 * g + 1][1])));
+      gv[g] = fmaxf(fmaxf(fabsf(YF(2 * g, 0)), fabsf(YF(2 * g, 1))), fmaxf(fabsf(YF(2 * g + 1, 0)), fabsf(YF(2 * g + 1, 1))));
     // reduce-scatter over the quad: lane q ends with groups 2q, 2q+1
     float w4[4], gq[2];
     {
@@ -480,20 +491,14 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int p = 0; p < 4; ++p) key[2 * p + j] = __shfl_sync(0xFFFFFFFFu, dkey[j], (lane & ~3) | p);
-    double d[8], d15[8];
     float df[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      if (MODE == M64_QUANT) {
-        d[g] = __dmul_rn(e4m3_val(key[g]), (double)scale32);
-        d15[g] = __dmul_rn(d[g], 1.5);
-        df[g] = (float)d[g];
-      } else {
-        df[g] = __uint_as_float(key[g]);
-        d[g] = (double)df[g];
-        d15[g] = (double)(df[g] * 1.5f);               // 5 significant bits: exact
-      }
-    }
+    for (int g = 0; g < 8; ++g)
+      df[g] = MODE == M64_QUANT ? (float)__dmul_rn(e4m3_val(key[g]), (double)scale32) : __uint_as_float(key[g]);
+    // exact float64 group scale (recomputed where needed to keep registers free)
+    auto dval = [&](int g) -> double {
+      return MODE == M64_QUANT ? __dmul_rn(e4m3_val(key[g]), (double)scale32) : (double)df[g];
+    };
 
     // --------------------------------------------------------------- codes
     // four packed code bytes per word: cw[j] holds blocks 4j..4j+3 (low nibble = even element)
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         float inv;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(df[g]));
         const float ilo = inv * (1.f - 0x1p-19f), ihi = inv * (1.f + 0x1p-19f);
-        const uint64_t y2 = f2pack(yf[k][0], yf[k][1]);
+        const uint64_t y2 = f2pack(YF(k, 0), YF(k, 1));
         asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(lo2[i]) : "l"(y2), "l"(f2pack(ilo, ilo)));
         asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(hi2[i]) : "l"(y2), "l"(f2pack(ihi, ihi)));
       }
@@ -532,9 +537,10 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           const int k = 4 * j + i, g = k >> 1;
           uint32_t c = (cw[j] >> (8 * i)) & 0xFF;
           const bool bad_pair = ((diff >> (8 * i)) & 0xFF) != 0;
-          if (!(d[g] > 0.0)) c = 0;
+          const double dg = dval(g);
+          if (!(dg > 0.0)) c = 0;
           else if (bad_pair || !(df[g] >= 0x1p-125f && df[g] < 0x1p125f))
-            c = rtn_code_exact(y[k][0], d[g]) | (rtn_code_exact(y[k][1], d[g]) << 4);
+            c = rtn_code_exact(y[k][0], dg) | (rtn_code_exact(y[k][1], dg) << 4);
           w |= c << (8 * i);
         }
         cw[j] = w;
@@ -550,25 +556,30 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         double dq0, dq1;
         dqfn(k, cbk, dq0, dq1);
         const double pn0 = __dmul_rn(y[k][0], y[k][0]), pn1 = __dmul_rn(y[k][1], y[k][1]);
-        const double pd0 = __dmul_rn(y[k][0], dq0), pd1 = __dmul_rn(y[k][1], dq1);
+        const double pd0 = __dmul_rn(fabs(y[k][0]), fabs(dq0)), pd1 = __dmul_rn(fabs(y[k][1]), fabs(dq1));
         if (k == 0) { an[0] = pn0; an[1] = pn1; ad[0] = pd0; ad[1] = pd1; }
         else { an[0] = __dadd_rn(an[0], pn0); an[1] = __dadd_rn(an[1], pn1); ad[0] = __dadd_rn(ad[0], pd0); ad[1] = __dadd_rn(ad[1], pd1); }
       }
     };
     if (MODE == M64_POSTHOC && !slow) {
+      // (double)df by field move (E8M3 values: 4 significant bits, normal or 0 -> d * 0 = 0)
+      auto dgv_at = [&](int g) { return bitsd((uint64_t)(((__float_as_uint(df[g]) & 0x7FFFFFFFu) >> 3) + 0x38000000u) << 32); };
       eden([&](int k, uint32_t cbk, double& dq0, double& dq1) {
-        uint32_t h2;
-        asm("{\n\t.reg .b8 t;\n\tcvt.u8.u32 t, %1;\n\tcvt.rn.f16x2.e2m1x2 %0, t;\n\t}" : "=r"(h2) : "r"(cbk));
-        float f0, f1;
-        asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-            : "=f"(f0), "=f"(f1) : "r"(h2));
-        dq0 = (double)(f0 * df[k >> 1]);
-        dq1 = (double)(f1 * df[k >> 1]);
+        // |FP4| as float64 high words from byte tables (PRMT), times d (exact)
+        const uint32_t sel = cbk & 0x77u;
+        const uint32_t t3 = __byte_perm(0x3F3F3F00u, 0x40404040u, sel);   // exponent byte
+        const uint32_t t2 = __byte_perm(0xF8F0E000u, 0x18100800u, sel);   // next byte
+        const double f0 = bitsd((uint64_t)__byte_perm(t3, t2, 0x0422u) << 32);
+        const double f1 = bitsd((uint64_t)__byte_perm(t3, t2, 0x1522u) << 32);
+        const double dgk = dgv_at(k >> 1);
+        dq0 = __dmul_rn(f0, dgk);
+        dq1 = __dmul_rn(f1, dgk);
       });
     } else {
       eden([&](int k, uint32_t cbk, double& dq0, double& dq1) {
-        dq0 = fp4_times(cbk & 0xF, d[k >> 1], d15[k >> 1]);
-        dq1 = fp4_times(cbk >> 4, d[k >> 1], d15[k >> 1]);
+        const double dg = dval(k >> 1), dg15 = __dmul_rn(dg, 1.5);
+        dq0 = fp4_times(cbk & 0xF, dg, dg15);
+        dq1 = fp4_times(cbk >> 4, dg, dg15);
       });
     }
     double num = __dadd_rn(an[0], an[1]), den = __dadd_rn(ad[0], ad[1]);
@@ -630,6 +641,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     if (MODE != M64_QUANT && wabs) atomicMax(&a.red[0], (unsigned long long)wabs);
     if ((MODE == M64_PMAX || MODE == M64_POSTHOC) && wp) atomicMax(&a.red[1], (unsigned long long)wp);
   }
+  if (SCALED && ((m16 & 0xFFFFu) >= 0x7F80u || (m16 >> 16) >= 0x7F80u)) bad = true;
   if (bad) atomic_or_err(a.err, Q2_ERR_NONFINITE);
   if (ovf) atomic_or_err(a.err, MODE == M64_QUANT ? Q2_ERR_SCALE448 : Q2_ERR_E8M3_OVF);
   if (nanscale) atomic_or_err(a.err, Q2_ERR_NAN_SCALE);
