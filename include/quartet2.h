@@ -22,17 +22,16 @@
  * NVFP4 tensor in HBM (q2_nvfp4): a logical [R, K] tensor quantized along K.
  *  codes   uint8 [R, K/2], row-major, two E2M1 codes per byte, low nibble =
  *          even k (the NV4T packing of quantizers.py:339).
- *  sf      UE4M3 group scales (one per 16 along K) stored as the TMEM image of a
- *          tcgen05.cp.128x256b copy: one 4 KiB block per (128-row block, pair of
- *          64-element K blocks), blocks K-fastest; rows padded to 128.  Block
- *          row L (TMEM lane) = 32 B: for K block h of the pair, bytes 16h+4q+i
- *          hold scale i of row 32q + L%32 (the MMA scale-vector layout, one
- *          replica per 32-lane subpartition), stored core-matrix major.  The
- *          primary byte of (r, j) is
- *            ((r/128)*ceil(K/128) + j/8)*4096 + ((r%32)/8)*256 + ((j/4)%2)*128
+ *  sf      UE4M3 group scales (one per 16 along K), unreplicated, in the tcgen05
+ *          block-scale vector layout: one 1 KiB block per (256-row block,
+ *          64-element K block), blocks K-fastest; rows padded to 256.  Block
+ *          byte (L/8)*256 + h*128 + (L%8)*16 + c*4 + i holds scale i of row
+ *          128*h + 32*c + L of the block (L = TMEM lane 0..31).  Each 512 B half
+ *          h is the shared-memory source of one tcgen05.cp.32x128b.warpx4, which
+ *          broadcasts it to the four TMEM subpartitions.  Byte of (r, j):
+ *            ((r/256)*ceil(K/64) + j/4)*1024 + ((r%32)/8)*256 + ((r/128)%2)*128
  *              + (r%8)*16 + ((r%128)/32)*4 + j%4
- *          and its replicas sit +1024, +2048, +3072 bytes later.
- *          Size: q2_sf_bytes(R, K) = ceil(R/128)*ceil(K/128)*4096.
+ *          Size: q2_sf_bytes(R, K) = ceil(R/256)*ceil(K/64)*1024.
  *  scale32 float32 device scalar (the reference's np.float32 tensor scale).
  */
 #ifndef QUARTET2_H_
@@ -63,7 +62,7 @@ typedef struct {
   int64_t  R, K;
 } q2_nvfp4;
 
-/* Bytes of the swizzled scale-factor buffer for a [R, K] tensor. */
+/* Bytes of the scale-factor buffer for a [R, K] tensor. */
 size_t q2_sf_bytes(int64_t R, int64_t K);
 
 /* Library build info (arch string); used by the loader's self-check. */
@@ -144,7 +143,8 @@ int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const 
 
 /* NVFP4 "TN" GEMM on tcgen05 block-scaled MMAs (kind::mxf4nvf4, UE4M3 scales
  * per 16, FP32 accumulation in TMEM):  D[M, N] = alpha * A[M,K] . B[N,K]^T
- * with alpha = *a->scale32 * *b->scale32 (+ beta*D if accumulate).
+ * with alpha = *a->scale32 * *b->scale32 (+ beta*D if accumulate).  CTA pairs
+ * (cta_group::2) compute 256x256 tiles; M, N tails are masked by TMA.
  * Replaces gemm_emulated (linear_graph.py:190-205) for the fprop, dgrad and
  * wgrad GEMMs.  d_dtype Q2_BF16 or Q2_F32; d row stride ldd (elements).
  * K % 64 == 0; K/2 % 16 == 0.                                                */

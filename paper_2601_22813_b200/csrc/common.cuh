@@ -15,22 +15,21 @@ constexpr int GROUP = 16;
 constexpr int CHUNK = 128;
 
 // ---------------------------------------------------------------- layout ----
-// Group scales are stored as the TMEM image of a tcgen05.cp.128x256b copy:
-// one 4 KiB block per (128-row block, 128-column K pair), blocks K-fastest.
-// Block row L (= TMEM lane) holds 32 B = 8 TMEM columns: for K-block h of the
-// pair, columns 4h..4h+3 carry the four scales of rows 32q + L%32 (q = 0..3),
-// i.e. the MMA scale-vector layout with each 32-lane subpartition holding a
-// replica.  Stored core-matrix major (8 rows x 16 B) with LBO 128 B / SBO 256 B.
-// sf_offset returns the primary replica; replica t sits t*1024 bytes later.
-__host__ __device__ __forceinline__ int64_t kpairs(int64_t K) { return (K + 127) / 128; }
-__host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t j, int64_t kp) {
+// Group scales (UE4M3, one per 16 along K) are stored unreplicated in the
+// tcgen05 block-scale vector layout: one 1 KiB block per (256-row block,
+// 64-element K block), blocks K-fastest.  Block byte
+//   (L/8)*256 + half*128 + (L%8)*16 + c*4 + i      (L = TMEM lane 0..31)
+// holds scale i (= j%4) of row 128*half + 32*c + L.  Each half is the smem
+// source of one tcgen05.cp.32x128b.warpx4 (core matrices of 8 lanes x 16 B,
+// SBO 256 B), which broadcasts it to the four TMEM subpartitions.
+__host__ __device__ __forceinline__ int64_t sf_kblocks(int64_t K) { return (K + 63) / 64; }
+__host__ __device__ __forceinline__ int64_t sf_offset(int64_t r, int64_t j, int64_t kb) {
   const int64_t L = r & 31;
-  return (((r >> 7) * kp + (j >> 3)) << 12) + ((L >> 3) << 8) + (((j >> 2) & 1) << 7) + ((L & 7) << 4) +
+  return (((r >> 8) * kb + (j >> 2)) << 10) + ((L >> 3) << 8) + (((r >> 7) & 1) << 7) + ((L & 7) << 4) +
          (((r >> 5) & 3) << 2) + (j & 3);
 }
-__device__ __forceinline__ void sf_store(uint8_t* sf, int64_t r, int64_t j, int64_t kp, uint8_t v) {
-  uint8_t* p = sf + sf_offset(r, j, kp);
-  p[0] = v; p[1024] = v; p[2048] = v; p[3072] = v;
+__device__ __forceinline__ void sf_store(uint8_t* sf, int64_t r, int64_t j, int64_t kb, uint8_t v) {
+  sf[sf_offset(r, j, kb)] = v;
 }
 
 // ------------------------------------------------------------------ E2M1 ----

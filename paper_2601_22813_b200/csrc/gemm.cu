@@ -1,67 +1,107 @@
-// NVFP4 x NVFP4 "TN" GEMM on 5th-gen tensor cores (tcgen05, sm_100a).
+// NVFP4 x NVFP4 "TN" GEMM on 5th-gen tensor cores, CTA pairs (tcgen05
+// cta_group::2, sm_100a).
 //
 //   D[M, N] = (scale32_a * scale32_b) * sum_k A[m, k] * B[n, k]   (+ D if accumulate)
 //
 // Replaces gemm_emulated (linear_graph.py:190-205), which dequantizes both
 // operands to float32 and runs an sgemm, for the three Quartet II GEMMs:
 // fprop Q(X).Q(W)^T, dgrad Q(E).Q(W^T)^T, wgrad Q(E^T).Q(X^T)^T.  Both operands
-// are E2M1 codes packed two per byte along K with one UE4M3 scale per 16,
-// which is exactly the operand format of tcgen05.mma kind::mxf4nvf4 with
-// block16 scaling.
+// are E2M1 codes packed two per byte along K with one UE4M3 scale per 16 --
+// the operand format of tcgen05.mma kind::mxf4nvf4 with block16 scaling.
 //
-// Persistent, warp-specialized (256 threads, one CTA per SM):
-//   warp 0  TMA producer: 128x256-fp4 slices of A and B (cp.async.bulk.tensor,
-//           128B swizzle) + their scale-factor atoms (cp.async.bulk) into a
-//           STAGES-deep ring guarded by full/empty mbarriers.
-//   warp 1  MMA issuer (one thread): tcgen05.cp scale atoms smem->TMEM, four
-//           tcgen05.mma (K = 64) per stage into one of two 128x128 fp32 TMEM
-//           accumulators; tcgen05.commit releases smem stages and signals the
-//           epilogue.
-//   warp 2  owns the TMEM allocation.
-//   warps 4-7  epilogue: tcgen05.ld the accumulator, scale, convert, write a
-//           128B-swizzled smem tile, TMA-store it (TMA reduce-add when
-//           accumulating).  The second accumulator lets the MMAs of the next
-//           tile run under this epilogue.
-// Tiles are visited in M-groups of 8 so concurrently running CTAs share B and A
-// tiles in L2.
+// Why CTA pairs: at 128x128 tiles the kernel streamed ~6300 B/clk out of L2
+// (the chip's LTS limit, B300_MICROARCH.md) for 2.2 PFLOP/s.  A pair computes a
+// 256x256 tile with one M=256, N=256 MMA per K=64 step: each CTA stages half of
+// A and half of B (its 128 rows of each) and the tensor cores read both CTAs'
+// shared memory, so operand bytes per FLOP halve; the scale factors are fetched
+// unreplicated and broadcast to the four TMEM subpartitions by
+// tcgen05.cp.32x128b.warpx4.
+//
+// Per CTA (384 threads, one CTA per SM, clusters of 2):
+//   warp 0   TMA producer: A/B slices (128 B of K x 128 rows, 128B swizzle) and
+//            the scale-factor halves, all completing on the LEADER's full
+//            barrier (cta_group::2 TMA).
+//   warp 1   (leader only) MMA issuer: 3 scale copies + 1 tcgen05.mma per K=64;
+//            commits release both CTAs' stages and signal both epilogues.
+//   warp 2   owns the TMEM allocation (cta_group::2, 512 columns).
+//   warps 4-11 epilogue: warp 4+e drains TMEM lanes 32*(e%4).. of columns
+//            128*(e/4)..+127 into registers, releases the accumulator (leader's
+//            barrier, 16 arrivals), then scales, converts and TMA-stores
+//            (TMA reduce-add when accumulating).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "tc_common.cuh"
 
 namespace q2 {
 
-constexpr int BM = 128, BN = 128, BKB = 128;             // BK = 256 fp4 = 128 bytes
-constexpr int A_STAGE = BM * BKB;                         // 16 KB
-constexpr int B_STAGE = BN * BKB;                         // 16 KB
-constexpr int SF_STAGE = 2 * 4096;                        // two 128x256b TMEM-image blocks (K pairs)
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE + 2 * SF_STAGE;
+constexpr int PT = 256;                                   // pair tile (M and N)
+constexpr int BKB = 128;                                  // K bytes per stage (256 fp4)
+constexpr int A_ST = 128 * BKB, B_ST = 128 * BKB;         // 16 KB each
+constexpr int SFA_ST = 2048, SFB_ST = 4096;               // 4 K64 blocks: CTA half / both halves
+constexpr int STAGE = A_ST + B_ST + SFA_ST + SFB_ST;      // 38 KB
+constexpr int STAGES = 4;
+constexpr int STG_BYTES = 16384;                          // one TMA-store box (128 rows x 128 B)
+constexpr int OFF_STG = STAGES * STAGE;                   // 2 groups x 2 boxes
+constexpr int OFF_BAR = OFF_STG + 4 * STG_BYTES;
+constexpr int GEMM_SMEM = OFF_BAR + 256 + 1024;
+constexpr int GEMM_THREADS = 384;
 constexpr int TMEM_COLS = 512;
-constexpr int SFA_COL = 256, SFB_COL = 272;               // after two 128-column accumulators
-constexpr int GEMM_THREADS = 256;
+constexpr int SFA_COL = 256, SFB_COL = 272;               // after the 256-column accumulator
 constexpr int GROUP_M = 8;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;               // shared::cluster address of the leader's copy
 
-template <bool F32>
-struct GemmCfg {
-  static constexpr int STAGES = F32 ? 3 : 4;
-  static constexpr int OUT_BYTES = BM * BN * (F32 ? 4 : 2);          // staging for the TMA store
-  static constexpr int OFF_OUT = STAGES * STAGE_BYTES;
-  static constexpr int OFF_BAR = OFF_OUT + OUT_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int BOX_COLS = F32 ? 32 : 64;                     // 128-byte store boxes
-};
-
-// instruction descriptor, kind::mxf4nvf4 (cute InstrDescriptorBlockScaled):
-// a/b format E2M1 (=1) at [7,10)/[10,13), K-major, N>>3 at [17,23),
-// scale format UE4M3 (=0) at [23], M>>4 at [24,29).
-constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor, kind::mxf4nvf4 (cute InstrDescriptorBlockScaled): a/b E2M1 (=1)
+// at [7,10)/[10,13), K-major, N>>3 at [17,23), scale UE4M3 (=0), M>>4 at [24,29).
+constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)(PT >> 3) << 17) | ((uint32_t)(PT >> 4) << 24);
 
 struct GemmArgs {
-  const uint8_t* sfa; const uint8_t* sfb;
   const float* sa; const float* sb;
-  int M, N, K;
-  int tiles_m, tiles_n;
+  int M, N, K, kb;                                        // kb = ceil(K/64) scale blocks per row block
+  int tiles_m, tiles_n, nk;
   int accumulate;
 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & PEER_MASK) : "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & PEER_MASK) : "memory");
+}
+__device__ __forceinline__ void tc2_cp_sf(uint32_t tmem, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(tmem), "l"(desc) : "memory");
+}
+__device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tsfa,
+                                        uint32_t tsfb, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %6, [%4], [%5], p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(accum), "r"(tsfa), "r"(tsfb), "r"(IDESC)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_commit(uint32_t bar) {   // arrive on `bar` in both CTAs of the pair
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"((unsigned short)3) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
+}
+// scale-factor source descriptor: core matrices of 8 lanes x 16 B, `sbo` bytes apart
+__device__ __forceinline__ uint64_t desc_sf32(uint32_t saddr, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
   const int per_group = GROUP_M * tiles_n;
@@ -73,168 +113,182 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     nvfp4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                       const __grid_constant__ CUtensorMap tmD, GemmArgs g) {
-  using C = GemmCfg<F32>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nsub_total = g.K / 64;                   // K = 64 MMAs
-  const int nk = (nsub_total + 3) / 4;
-  const int64_t kpr = (g.K + 127) / 128;             // scale image blocks per 128-row block
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int ntiles = g.tiles_m * g.tiles_n;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + C::STAGES);
-  const uint32_t bar_accf = smem_u32(bars + 2 * C::STAGES), bar_acce = smem_u32(bars + 2 * C::STAGES + 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + STAGES);
+  const uint32_t bar_accf = smem_u32(bars + 2 * STAGES), bar_acce = smem_u32(bars + 2 * STAGES + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(bar_full + 8 * s, 1); mbar_init(bar_empty + 8 * s, 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(bar_accf + 8 * s, 1); mbar_init(bar_acce + 8 * s, 4); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(bar_full + 8 * s, 1); mbar_init(bar_empty + 8 * s, 1); }
+    mbar_init(bar_accf, 1);
+    mbar_init(bar_acce, 16);                                  // 8 epilogue warps x 2 CTAs
     mbar_fence_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSFA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSFB)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmD)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(TMEM_COLS)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();                                             // barriers and TMEM of both CTAs ready
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producer (both CTAs) ----------------
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = pair; t < ntiles; t += npairs) {
         int tm, tn;
         tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
-          const int s = it % C::STAGES;
-          if (it >= C::STAGES) mbar_wait(bar_empty + 8 * s, ((it / C::STAGES) - 1) & 1);
-          const int nkp = (int)(kpr - 2 * kt < 2 ? kpr - 2 * kt : 2);
-          unsigned char* st = smem + s * STAGE_BYTES;
-          mbar_expect_tx(bar_full + 8 * s, A_STAGE + B_STAGE + 2 * nkp * 4096);
-          tma_load_2d(smem_u32(st), &tmA, kt * BKB, m0, bar_full + 8 * s);
-          tma_load_2d(smem_u32(st + A_STAGE), &tmB, kt * BKB, n0, bar_full + 8 * s);
-          bulk_load(smem_u32(st + A_STAGE + B_STAGE), g.sfa + (((int64_t)tm * kpr + 2 * kt) << 12), nkp * 4096,
-                    bar_full + 8 * s);
-          bulk_load(smem_u32(st + A_STAGE + B_STAGE + SF_STAGE), g.sfb + (((int64_t)tn * kpr + 2 * kt) << 12),
-                    nkp * 4096, bar_full + 8 * s);
+        const int m0 = tm * PT + (int)rank * 128, n0 = tn * PT + (int)rank * 128;
+        for (int kt = 0; kt < g.nk; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
+          const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s;
+          if (rank == 0) mbar_expect_tx(fb, 2 * STAGE);
+          tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
+          tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
+          tma2_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, fb);
+          tma2_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, fb);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    if (rank == 0 && lane == 0) {
+      // ---------------- MMA issuer (leader) ----------------
       int it = 0, tc = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc) {
-        const int as = tc & 1;
-        if (tc >= 2) mbar_wait(bar_acce + 8 * as, ((tc >> 1) - 1) & 1);   // epilogue drained this accumulator
+      for (int t = pair; t < ntiles; t += npairs, ++tc) {
+        if (tc >= 1) mbar_wait(bar_acce, (tc - 1) & 1);       // both epilogues drained the accumulator
         tc_fence_after();
-        const uint32_t dacc = tmem + as * BN;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
-          const int s = it % C::STAGES;
-          mbar_wait(bar_full + 8 * s, (it / C::STAGES) & 1);
+        for (int kt = 0; kt < g.nk; ++kt, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
           tc_fence_after();
-          const int nsub = min(4, nsub_total - kt * 4);
-          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-          for (int p = 0; p < (nsub + 1) / 2; ++p) {
-            tc_cp_sf(tmem + SFA_COL + 8 * p, desc_sf(st + A_STAGE + B_STAGE + p * 4096));
-            tc_cp_sf(tmem + SFB_COL + 8 * p, desc_sf(st + A_STAGE + B_STAGE + SF_STAGE + p * 4096));
+          const uint32_t st = smem_u32(smem + s * STAGE);
+          const uint32_t sfa = st + A_ST + B_ST, sfb = sfa + SFA_ST;
+          const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_ST);
+          const int nsub = min(4, g.K / 64 - 4 * kt);          // K tail: no MMA reads scales beyond K
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (kk >= nsub) break;
+            tc2_cp_sf(tmem + SFA_COL + 4 * kk, desc_sf32(sfa + 512 * kk, 128));
+            tc2_cp_sf(tmem + SFB_COL + 8 * kk, desc_sf32(sfb + 1024 * kk, 256));
+            tc2_cp_sf(tmem + SFB_COL + 8 * kk + 4, desc_sf32(sfb + 1024 * kk + 128, 256));
+            tc2_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk,
+                    (kt | kk) != 0);
           }
-          const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_STAGE);
-          for (int kk = 0; kk < nsub; ++kk)
-            tc_mma(dacc, adesc + 2 * kk, bdesc + 2 * kk, IDESC, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 4 * kk,
-                   (kt | kk) != 0);
-          tc_commit(bar_empty + 8 * s);
+          tc2_commit(bar_empty + 8 * s);
         }
-        tc_commit(bar_accf + 8 * as);
+        tc2_commit(bar_accf);
       }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
-    const int ew = warp - 4;                       // TMEM lanes 32*ew .. 32*ew+31
-    const int row = ew * 32 + lane;                // row within the tile
+    const int e = warp - 4, sp = e & 3, grp = e >> 2;
+    const int row = sp * 32 + lane;                           // row within the CTA's 128
     const float alpha = __ldg(g.sa) * __ldg(g.sb);
-    unsigned char* out = smem + C::OFF_OUT;
-    constexpr int NBOX = BN / C::BOX_COLS;
+    unsigned char* stg = smem + OFF_STG + grp * 2 * STG_BYTES;
+    const uint32_t tbase = tmem + ((uint32_t)(sp * 32) << 16) + grp * 128;
     int tc = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc) {
+    for (int t = pair; t < ntiles; t += npairs, ++tc) {
       int tm, tn;
       tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
-      const int as = tc & 1;
-      mbar_wait(bar_accf + 8 * as, (tc >> 1) & 1);
+      mbar_wait(bar_accf, tc & 1);
       tc_fence_after();
-      if (threadIdx.x == 128 && tc > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      named_bar(1, 128);                            // staging buffer free again
+      uint32_t v[4][32];
 #pragma unroll
-      for (int q = 0; q < BN / 32; ++q) {
-        uint32_t r[32];
-        Q2_LD32(r, tmem + ((uint32_t)(ew * 32) << 16) + as * BN + q * 32);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (F32) {
-          // 32 fp32 = 128 B = one full swizzled row of box q
-          unsigned char* base = out + q * (BM * 128) + row * 128;
-#pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
-            const float4 v = make_float4(alpha * __uint_as_float(r[4 * ch]), alpha * __uint_as_float(r[4 * ch + 1]),
-                                         alpha * __uint_as_float(r[4 * ch + 2]), alpha * __uint_as_float(r[4 * ch + 3]));
-            *reinterpret_cast<float4*>(base + ((ch ^ (row & 7)) << 4)) = v;
-          }
-        } else {
-          // 32 bf16 = 64 B = half a swizzled row of box q/2
-          unsigned char* base = out + (q >> 1) * (BM * 128) + row * 128;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t p[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(r[8 * ch + 2 * e]),
-                                                       alpha * __uint_as_float(r[8 * ch + 2 * e + 1]));
-              p[e] = *reinterpret_cast<uint32_t*>(&h);
-            }
-            const int chunk = (q & 1) * 4 + ch;
-            *reinterpret_cast<uint4*>(base + ((chunk ^ (row & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
-          }
-        }
-      }
+      for (int q = 0; q < 4; ++q) Q2_LD32(v[q], tbase + q * 32);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_acce + 8 * as);   // MMA warp may reuse this accumulator
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, 128);
-      if (threadIdx.x == 128) {
+      if (lane == 0) mbar_arrive_leader(bar_acce);            // MMA may overwrite the accumulator
+      const int gm0 = tm * PT + (int)rank * 128, gn0 = tn * PT + grp * 128;
+      constexpr int PASSES = F32 ? 2 : 1;                     // 32 KB of output per pass
 #pragma unroll
-        for (int b = 0; b < NBOX; ++b)
-          tma_store_2d(&tmD, smem_u32(out + b * (BM * 128)), tn * BN + b * C::BOX_COLS, tm * BM, g.accumulate != 0);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      for (int pass = 0; pass < PASSES; ++pass) {
+        if (lane == 0 && sp == 0 && (tc > 0 || pass > 0)) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        named_bar(1 + grp, 128);                              // staging free
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {                         // box b of this pass: 128 rows x 128 B
+          unsigned char* base = stg + b * STG_BYTES + row * 128;
+          if (F32) {
+            const uint32_t* r = v[2 * pass + b];              // 32 fp32 columns
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              *reinterpret_cast<float4*>(base + ((ch ^ (row & 7)) << 4)) =
+                  make_float4(alpha * __uint_as_float(r[4 * ch]), alpha * __uint_as_float(r[4 * ch + 1]),
+                              alpha * __uint_as_float(r[4 * ch + 2]), alpha * __uint_as_float(r[4 * ch + 3]));
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {                  // 64 bf16 columns: v[2b], v[2b+1]
+              const uint32_t* r = v[2 * b + (ch >> 2)] + 8 * (ch & 3);
+              uint32_t p[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(r[2 * i]), alpha * __uint_as_float(r[2 * i + 1]));
+                p[i] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              *reinterpret_cast<uint4*>(base + ((ch ^ (row & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar(1 + grp, 128);
+        if (lane == 0 && sp == 0) {
+          constexpr int BC = F32 ? 32 : 64;                   // columns per box
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            tma_store_2d(&tmD, smem_u32(stg + b * STG_BYTES), gn0 + (2 * pass + b) * BC, gm0, g.accumulate != 0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
-    if (threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (lane == 0 && sp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();                                             // peer's MMAs/arrivals done before teardown
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
 }
 
+static bool make_sf_map(CUtensorMap* map, const void* sf, int64_t R, int64_t K, uint32_t halves) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  const uint64_t groups = (uint64_t)((R + 255) / 256) * (uint64_t)sf_kblocks(K) * 4;
+  cuuint64_t dims[3] = {128, 2, (cuuint64_t)groups};
+  cuuint64_t strides[2] = {128, 256};
+  cuuint32_t box[3] = {128, halves, 16};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(sf), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <bool F32>
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md, const GemmArgs& g,
-                       cudaStream_t st) {
-  using C = GemmCfg<F32>;
+static int launch_gemm(const CUtensorMap* maps, const GemmArgs& g, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(nvfp4_gemm_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+    if (cudaFuncSetAttribute(nvfp4_gemm_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) !=
         cudaSuccess)
       return Q2_ECUDA;
     attr = true;
@@ -243,7 +297,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUten
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = g.tiles_m * g.tiles_n;
-  nvfp4_gemm_kernel<F32><<<std::min(ntiles, nsm), GEMM_THREADS, C::SMEM, st>>>(ma, mb, md, g);
+  const int npairs = std::max(1, std::min(ntiles, nsm / 2));
+  nvfp4_gemm_kernel<F32><<<2 * npairs, GEMM_THREADS, GEMM_SMEM, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], g);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
 }
@@ -260,14 +315,15 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
   const int esz = d_dtype == Q2_F32 ? 4 : 2;
   if (ldd < b->R || (ldd * esz) % 16 || (reinterpret_cast<uintptr_t>(d) & 15)) return Q2_EINVAL;
   if (a->R > INT32_MAX || b->R > INT32_MAX || a->K > INT32_MAX) return Q2_EINVAL;
-  CUtensorMap ma, mb, md;
-  if (!make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, a->codes, a->K / 2, a->R, a->K / 2, BKB, BM) ||
-      !make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_UINT8, b->codes, b->K / 2, b->R, b->K / 2, BKB, BN) ||
-      !make_map(&md, d_dtype == Q2_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d,
-                b->R, a->R, ldd * esz, d_dtype == Q2_F32 ? 32 : 64, BM))
+  CUtensorMap maps[5];
+  if (!make_map(&maps[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, a->codes, a->K / 2, a->R, a->K / 2, BKB, 128) ||
+      !make_map(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, b->codes, b->K / 2, b->R, b->K / 2, BKB, 128) ||
+      !make_sf_map(&maps[2], a->sf, a->R, a->K, 1) || !make_sf_map(&maps[3], b->sf, b->R, b->K, 2) ||
+      !make_map(&maps[4], d_dtype == Q2_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d,
+                b->R, a->R, ldd * esz, d_dtype == Q2_F32 ? 32 : 64, 128))
     return Q2_ECUDA;
-  GemmArgs g{a->sf, b->sf, a->scale32, b->scale32, (int)a->R, (int)b->R, (int)a->K,
-             (int)((a->R + BM - 1) / BM), (int)((b->R + BN - 1) / BN), accumulate};
+  GemmArgs g{a->scale32, b->scale32, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
+             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d_dtype == Q2_F32 ? launch_gemm<true>(ma, mb, md, g, st) : launch_gemm<false>(ma, mb, md, g, st);
+  return d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
 }

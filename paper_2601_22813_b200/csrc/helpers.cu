@@ -11,7 +11,7 @@ __global__ void dequant_kernel(const uint8_t* __restrict__ codes, const uint8_t*
   const int64_t gpr = K / GROUP, g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= R * gpr) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  const double d = __dmul_rn(e4m3_val(sf[sf_offset(r, j, kpairs(K))]), (double)*scale32);
+  const double d = __dmul_rn(e4m3_val(sf[sf_offset(r, j, sf_kblocks(K))]), (double)*scale32);
   const uint2 c = *reinterpret_cast<const uint2*>(codes + r * (K / 2) + j * 8);
   double* o = out + r * K + j * GROUP;
 #pragma unroll
@@ -26,7 +26,7 @@ __global__ void unpack_kernel(const uint8_t* __restrict__ codes, const uint8_t* 
   const int64_t gpr = K / GROUP, g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= R * gpr) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  s8[g] = sf[sf_offset(r, j, kpairs(K))];
+  s8[g] = sf[sf_offset(r, j, sf_kblocks(K))];
   const uint2 c = *reinterpret_cast<const uint2*>(codes + r * (K / 2) + j * 8);
 #pragma unroll
   for (int k = 0; k < 16; ++k) fp4[r * K + j * GROUP + k] = ((k < 8 ? c.x : c.y) >> (4 * (k & 7))) & 0xF;
@@ -37,7 +37,7 @@ __global__ void pack_kernel(const uint8_t* __restrict__ fp4, const uint8_t* __re
   const int64_t gpr = K / GROUP, g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= R * gpr) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  sf_store(sf, r, j, kpairs(K), s8[g]);
+  sf_store(sf, r, j, sf_kblocks(K), s8[g]);
   uint32_t lo = 0, hi = 0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {

@@ -38,7 +38,7 @@ __global__ void posthoc2_kernel(const uint16_t* __restrict__ pseudo, const doubl
   if (g == 0) *scale32_out = scale32;
   if (g >= total) return;
   const int64_t r = g / gpr, j = g - r * gpr;
-  const int64_t kpr = kpairs(K);
+  const int64_t kpr = sf_kblocks(K);
   if (pmax == 0.0) { sf_store(sf, r, j, kpr, 0); return; }
   const double ps = (double)__uint_as_float((uint32_t)pseudo[g] << 16);
   const double shifted = __ddiv_rn(ps, (double)scale32);

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-      const int64_t kp = kpairs(a.R);
+      const int64_t kb = sf_kblocks(a.R);
       int it = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 16384, &tm, tr * M64_ROWS + j * 32, tc * CHUNK, fb);
         } else {
           tma_load_2d(dst, &tm, tr * 32, tc * CHUNK, fb);                  // codes [128 tape rows x 32 B]
-          bulk_load(dst + 4096, a.tape_sf + (((int64_t)tc * kp + (tr >> 1)) << 12), 1024, fb);
+          bulk_load(dst + 4096, a.tape_sf + ((((int64_t)tc >> 1) * kb + tr) << 10), 1024, fb);
         }
       }
     }
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         const uint4 cw = *reinterpret_cast<const uint4*>(smem + s * TL::RAW + tri * 32 + h * 16);
         const int L = tri & 31;
         const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + s * TL::RAW + 4096 + ((L >> 3) << 8) +
-                                                                ((tr & 1) << 7) + ((L & 7) << 4) + ((tri >> 5) << 2));
+                                                                ((tc & 1) << 7) + ((L & 7) << 4) + ((tri >> 5) << 2));
         const uint32_t neg = ((a.sign[tri >> 5] >> (tri & 31)) & 1u) ? 0x80008000u : 0u;
         uint32_t sc[2];
 #pragma unroll
@@ -625,8 +625,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         if (a.corr && q == 0) a.corr[r * (a.K / CHUNK) + tc] = S;
       } else if ((q & 1) == 0) {                      // lanes 2m: the 4-scale word of groups 4m..4m+3
         const uint32_t word = half | (other << 16);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(a.sf + sf_offset(r, (int64_t)tc * 8 + 2 * q, kpairs(a.K)));
-        dst[0] = word; dst[256] = word; dst[512] = word; dst[768] = word;
+        *reinterpret_cast<uint32_t*>(a.sf + sf_offset(r, (int64_t)tc * 8 + 2 * q, sf_kblocks(a.K))) = word;
       }
     }
   }
@@ -661,7 +660,7 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
   if (tq == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
   if (tq >= total) return;
   const int64_t r = tq / qpr, jq = tq - r * qpr;
-  uint32_t* dst = reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, kpairs(K)));
+  uint32_t* dst = reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, sf_kblocks(K)));
   uint32_t word = 0;
   bool ovf = false;
   if (pmax > 0.0) {
@@ -670,7 +669,7 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
            (aword_code(w.y & 0xFFFF, k, &ovf) << 16) | (aword_code(w.y >> 16, k, &ovf) << 24);
   }
   if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
-  dst[0] = word; dst[256] = word; dst[512] = word; dst[768] = word;
+  *dst = word;
 }
 
 }  // namespace q2

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(QT + 32, 2) quant_fwd_kernel(
   extern __shared__ __align__(128) unsigned char qsm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(qsm + QNST * QT * GB);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + QNST);
-  const int64_t gpr = K / GROUP, total = R * gpr, kpr = kpairs(K);
+  const int64_t gpr = K / GROUP, total = R * gpr, kpr = sf_kblocks(K);
   const int64_t nunits = (total + QT - 1) / QT;
   if (threadIdx.x == 0) {
     for (int s = 0; s < QNST; ++s) { mbar_init(full0 + 8 * s, 1); mbar_init(empty0 + 8 * s, QT / 32); }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(128) quant_fix_kernel(const void* __restrict__
   const uint32_t n = *fix_count;
   const float amax = __uint_as_float(*amax_bits);
   const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
-  const int64_t gpr = K / GROUP, kpr = kpairs(K);
+  const int64_t gpr = K / GROUP, kpr = sf_kblocks(K);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t gid = fix_list[i];
     const uint32_t r = fgpr.div(gid), j = gid - r * (uint32_t)gpr;
@@ -416,7 +416,7 @@ using namespace q2;
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 extern "C" size_t q2_sf_bytes(int64_t R, int64_t K) {
-  return (size_t)((R + 127) / 128) * (size_t)kpairs(K) * 4096u;
+  return (size_t)((R + 255) / 256) * (size_t)sf_kblocks(K) * 1024u;
 }
 
 extern "C" const char* q2_version(void) { return "quartet2-b200 sm_100a"; }

@@ -112,7 +112,7 @@ class NVFP4Tensor:
         R = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
         K = shape[-1]
         nsf = _lib.lib().q2_sf_bytes(R, K)
-        # Scale padding (rows beyond R in the last 128-row atom) only feeds GEMM
+        # Scale padding (rows beyond R in the last 256-row block) only feeds GEMM
         # outputs that are masked, so the buffer needs no zero fill.
         return cls(torch.empty((R, K // 2), dtype=torch.uint8, device=device),
                    torch.empty(nsf, dtype=torch.uint8, device=device),

@@ -27,9 +27,6 @@ def _dev(x, bf16=True):
 
 
 def assert_same(gpu_t, ref_t, what=""):
-    if gpu_t.R % 128 == 0 and gpu_t.K % 128 == 0:       # every scale byte has 4 identical TMEM-lane replicas
-        blocks = gpu_t.sf.cpu().numpy().reshape(-1, 4, 1024)
-        assert (blocks == blocks[:, :1]).all(), f"{what} scale replicas disagree"
     fp4, s8, s32 = gpu_t.to_reference()
     assert np.float32(s32).tobytes() == np.float32(ref_t.scale32).tobytes(), f"{what} scale32 {s32!r} vs {ref_t.scale32!r}"
     bad_s = np.argwhere(s8 != ref_t.scales8)

@@ -27,10 +27,10 @@ def test_library_exports_header_symbols():
 def test_sf_bytes():
     from paper_2601_22813_b200 import _lib
     L = _lib.lib()
-    assert L.q2_sf_bytes(128, 64) == 4096
-    assert L.q2_sf_bytes(129, 64) == 8192
-    assert L.q2_sf_bytes(128, 256) == 8192
-    assert L.q2_sf_bytes(256, 80) == 2 * 4096
+    assert L.q2_sf_bytes(128, 64) == 1024
+    assert L.q2_sf_bytes(257, 64) == 2048
+    assert L.q2_sf_bytes(128, 256) == 4096
+    assert L.q2_sf_bytes(256, 80) == 2 * 1024
 
 
 def test_host_streams_match_oracle():
@@ -45,33 +45,28 @@ def test_host_streams_match_oracle():
 
 
 def test_sf_layout_formula():
-    """The scale image (include/quartet2.h) places every (row, group) at 4 distinct
-    replicas, covers each 4 KiB block exactly, and per TMEM lane L / column c holds
-    the scale of row 32*(c%4) + L%32 (the tcgen05 block-scale vector layout)."""
+    """The scale layout (include/quartet2.h) is a bijection onto the 1 KiB blocks,
+    and per block half (the source of one tcgen05.cp.32x128b.warpx4) TMEM lane L
+    / column c holds the scale of row 128*half + 32*c + L (the tcgen05
+    block-scale vector layout; one K=64 MMA block per 1 KiB)."""
     def off(r, j, K):
-        kp = (K + 127) // 128
+        kb = (K + 63) // 64
         L = r % 32
-        return (((r // 128) * kp + j // 8) * 4096 + (L // 8) * 256 + ((j // 4) % 2) * 128 + (L % 8) * 16
+        return (((r // 256) * kb + j // 4) * 1024 + (L // 8) * 256 + ((r // 128) % 2) * 128 + (L % 8) * 16
                 + ((r % 128) // 32) * 4 + j % 4)
-    K, R = 256, 256
-    seen = set()
-    for r in range(R):
-        for j in range(K // 16):
-            for t in range(4):
-                seen.add(off(r, j, K) + 1024 * t)
-    assert len(seen) == 4 * R * K // 16 and max(seen) < 4 * R * K // 16
-    # lane view: block byte b -> (lane, column, byte-in-column) of a 128x256b copy
-    def lane_col(b):
-        g, rest = divmod(b % 4096, 256)
+    K, R = 256, 512
+    seen = {off(r, j, K) for r in range(R) for j in range(K // 16)}
+    assert len(seen) == R * K // 16 and max(seen) < R * K // 16
+    def lane_col(b):                       # block byte -> (half, lane, column, byte-in-column)
+        g, rest = divmod(b % 1024, 256)
         half, rest = divmod(rest, 128)
         row8, byte = divmod(rest, 16)
-        return 8 * g + row8, 4 * half + byte // 4, byte % 4
-    for r in (0, 5, 37, 100, 127):
-        for j in (0, 3, 4, 7):
-            for t in range(4):
-                lane, col, i = lane_col(off(r, j, K) + 1024 * t)
-                assert lane % 32 == r % 32 and lane // 32 == t
-                assert col == 4 * ((j // 4) % 2) + (r % 128) // 32 and i == j % 4
+        return half, 8 * g + row8, byte // 4, byte % 4
+    for r in (0, 5, 37, 100, 127, 128, 200, 255, 300):
+        for j in (0, 3, 4, 7, 13):
+            half, lane, col, i = lane_col(off(r, j, K))
+            assert r % 256 == 128 * half + 32 * col + lane and i == j % 4
+            assert off(r, j, K) // 1024 == (r // 256) * (K // 64) + j // 4
 
 
 def test_layer_config_validation():
