@@ -13,21 +13,25 @@
 // (the chip's LTS limit, B300_MICROARCH.md) for 2.2 PFLOP/s.  A pair computes a
 // 256x256 tile with one M=256, N=256 MMA per K=64 step: each CTA stages half of
 // A and half of B (its 128 rows of each) and the tensor cores read both CTAs'
-// shared memory, so operand bytes per FLOP halve; the scale factors are fetched
-// unreplicated and broadcast to the four TMEM subpartitions by
-// tcgen05.cp.32x128b.warpx4.
+// shared memory, so operand bytes per FLOP halve.  Scale factors are fetched
+// unreplicated; instead of tcgen05.cp (three copies per MMA measured at ~45% of
+// the MMA time) four "scale warps" write them into TMEM with tcgen05.st, each
+// warp filling its own 32-lane subpartition (the replication the block-scaled
+// MMA needs comes for free), so the MMA thread issues only MMAs.
 //
-// Per CTA (384 threads, one CTA per SM, clusters of 2):
-//   warp 0   TMA producer: A/B slices (128 B of K x 128 rows, 128B swizzle) and
-//            the scale-factor halves, all completing on the LEADER's full
-//            barrier (cta_group::2 TMA).
-//   warp 1   (leader only) MMA issuer: 3 scale copies + 1 tcgen05.mma per K=64;
-//            commits release both CTAs' stages and signal both epilogues.
-//   warp 2   owns the TMEM allocation (cta_group::2, 512 columns).
-//   warps 4-11 epilogue: warp 4+e drains TMEM lanes 32*(e%4).. of columns
-//            128*(e/4)..+127 into registers, releases the accumulator (leader's
-//            barrier, 16 arrivals), then scales, converts and TMA-stores
-//            (TMA reduce-add when accumulating).
+// Per CTA (512 threads, one CTA per SM, clusters of 2):
+//   warp 0   TMA producer: A/B slices (128 B of K x 128 rows, 128B swizzle)
+//            complete on the LEADER's full barrier (cta_group::2 TMA); the raw
+//            scale halves complete on this CTA's scale barrier.
+//   warp 1   (leader only) MMA issuer: 4 tcgen05.mma per stage; commits
+//            release both CTAs' stages and signal both epilogues.
+//   warp 2   owns the TMEM allocation (cta_group::2, 512 columns: 256-column
+//            accumulator + one 48-column scale slot per stage).
+//   warps 4-7 scale warps (see above); arrive on the leader's scale-ready barrier.
+//   warps 8-15 epilogue: warp 8+e drains TMEM lanes 32*(e%4).. of columns
+//            128*(e/4)..+127 (two 64-column passes), releases the accumulator
+//            (leader's barrier, 16 arrivals), scales, converts and stores
+//            16-byte vectors straight to global (read-add-write when accumulating).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "tc_common.cuh"
@@ -37,16 +41,15 @@ namespace q2 {
 constexpr int PT = 256;                                   // pair tile (M and N)
 constexpr int BKB = 128;                                  // K bytes per stage (256 fp4)
 constexpr int A_ST = 128 * BKB, B_ST = 128 * BKB;         // 16 KB each
-constexpr int SFA_ST = 2048, SFB_ST = 4096;               // 4 K64 blocks: CTA half / both halves
+constexpr int SFA_ST = 2048;                              // 4 K64 blocks x the CTA's 512 B half
+constexpr int SFB_ST = 4096;                              // 4 K64 blocks x both halves
 constexpr int STAGE = A_ST + B_ST + SFA_ST + SFB_ST;      // 38 KB
-constexpr int STAGES = 4;
-constexpr int STG_BYTES = 16384;                          // one TMA-store box (128 rows x 128 B)
-constexpr int OFF_STG = STAGES * STAGE;                   // 2 groups x 2 boxes
-constexpr int OFF_BAR = OFF_STG + 4 * STG_BYTES;
+constexpr int STAGES = 5;
+constexpr int OFF_BAR = STAGES * STAGE;
 constexpr int GEMM_SMEM = OFF_BAR + 256 + 1024;
-constexpr int GEMM_THREADS = 384;
+constexpr int GEMM_THREADS = 512;
 constexpr int TMEM_COLS = 512;
-constexpr int SFA_COL = 256, SFB_COL = 272;               // after the 256-column accumulator
+constexpr int SF_COL = 256, SF_SLOT = 48;                 // per stage: 4 x (SFA 4 + SFB 8) columns
 constexpr int GROUP_M = 8;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;               // shared::cluster address of the leader's copy
 
@@ -56,6 +59,7 @@ constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)(PT >> 3) << 17) 
 
 struct GemmArgs {
   const float* sa; const float* sb;
+  void* d; int64_t ldd;
   int M, N, K, kb;                                        // kb = ceil(K/64) scale blocks per row block
   int tiles_m, tiles_n, nk;
   int accumulate;
@@ -79,8 +83,16 @@ __device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* ma
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar & PEER_MASK) : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+}
 __device__ __forceinline__ void tc2_cp_sf(uint32_t tmem, uint64_t desc) {
   asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(tmem), "l"(desc) : "memory");
+}
+__device__ __forceinline__ void tc2_cp_sf256(uint32_t tmem, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(tmem), "l"(desc) : "memory");
 }
 __device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tsfa,
                                         uint32_t tsfb, uint32_t accum) {
@@ -116,7 +128,7 @@ template <bool F32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     nvfp4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
-                      const __grid_constant__ CUtensorMap tmD, GemmArgs g) {
+                      GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -125,12 +137,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const int ntiles = g.tiles_m * g.tiles_n;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + STAGES);
-  const uint32_t bar_accf = smem_u32(bars + 2 * STAGES), bar_acce = smem_u32(bars + 2 * STAGES + 1);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2);
+  const uint32_t bar_full = smem_u32(bars);                   // A/B of both CTAs (leader's copy used)
+  const uint32_t bar_sff = smem_u32(bars + STAGES);           // this CTA's raw scales landed
+  const uint32_t bar_sfr = smem_u32(bars + 2 * STAGES);       // scales in TMEM, both CTAs (leader's copy)
+  const uint32_t bar_empty = smem_u32(bars + 3 * STAGES);     // stage (and its TMEM scale slot) free
+  const uint32_t bar_accf = smem_u32(bars + 4 * STAGES), bar_acce = smem_u32(bars + 4 * STAGES + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * STAGES + 2);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(bar_full + 8 * s, 1); mbar_init(bar_empty + 8 * s, 1); }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_sff + 8 * s, 1);
+      mbar_init(bar_sfr + 8 * s, 8);                          // 4 scale warps x 2 CTAs
+      mbar_init(bar_empty + 8 * s, 1);
+    }
     mbar_init(bar_accf, 1);
     mbar_init(bar_acce, 16);                                  // 8 epilogue warps x 2 CTAs
     mbar_fence_init();
@@ -138,7 +158,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSFA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSFB)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmD)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -161,13 +180,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int m0 = tm * PT + (int)rank * 128, n0 = tn * PT + (int)rank * 128;
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
-          const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s;
-          if (rank == 0) mbar_expect_tx(fb, 2 * STAGE);
+          if (it >= STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
+          const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s, sb = bar_sff + 8 * s;
+          if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST));
           tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
           tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
-          tma2_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, fb);
-          tma2_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, fb);
+          mbar_expect_tx(sb, SFA_ST + SFB_ST);
+          tma_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, sb);
+          tma_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, sb);
         }
       }
     }
@@ -181,87 +201,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
           mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
+          mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE);
-          const uint32_t sfa = st + A_ST + B_ST, sfb = sfa + SFA_ST;
           const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_ST);
-          const int nsub = min(4, g.K / 64 - 4 * kt);          // K tail: no MMA reads scales beyond K
+          const uint32_t tsf = tmem + SF_COL + SF_SLOT * s;
+          const int nsub = min(4, g.K / 64 - 4 * kt);          // K tail: no MMA past K
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             if (kk >= nsub) break;
-            tc2_cp_sf(tmem + SFA_COL + 4 * kk, desc_sf32(sfa + 512 * kk, 128));
-            tc2_cp_sf(tmem + SFB_COL + 8 * kk, desc_sf32(sfb + 1024 * kk, 256));
-            tc2_cp_sf(tmem + SFB_COL + 8 * kk + 4, desc_sf32(sfb + 1024 * kk + 128, 256));
-            tc2_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk,
-                    (kt | kk) != 0);
+            tc2_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, tsf + 12 * kk, tsf + 12 * kk + 4, (kt | kk) != 0);
           }
           tc2_commit(bar_empty + 8 * s);
         }
         tc2_commit(bar_accf);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- scale warps: raw scales -> TMEM (both CTAs) ----------------
+    // Warp 4+sp writes TMEM lanes 32sp..32sp+31, i.e. one replica of every
+    // scale vector; lane L holds rows 32c + L (c = column within a 4-group).
+    const int sp = warp - 4;
+    const uint32_t trow = (uint32_t)(sp * 32) << 16;
+    int it = 0;
+    for (int t = pair; t < ntiles; t += npairs) {
+      for (int kt = 0; kt < g.nk; ++kt, ++it) {
+        const int s = it % STAGES;
+        mbar_wait_sleep(bar_sff + 8 * s, (it / STAGES) & 1);
+        const unsigned char* sfa = smem + s * STAGE + A_ST + B_ST;
+        const unsigned char* sfb = sfa + SFA_ST;
+        const uint32_t tsf = tmem + trow + SF_COL + SF_SLOT * s;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint4 a4 = *reinterpret_cast<const uint4*>(sfa + 512 * kk + (lane >> 3) * 128 + (lane & 7) * 16);
+          const uint4 b0 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + (lane & 7) * 16);
+          const uint4 b1 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + 128 + (lane & 7) * 16);
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+                       ::"r"(tsf + 12 * kk), "r"(a4.x), "r"(a4.y), "r"(a4.z), "r"(a4.w) : "memory");
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                       ::"r"(tsf + 12 * kk + 4), "r"(b0.x), "r"(b0.y), "r"(b0.z), "r"(b0.w), "r"(b1.x), "r"(b1.y),
+                       "r"(b1.z), "r"(b1.w) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(bar_sfr + 8 * s);
+      }
+    }
+  } else if (warp >= 8) {
     // ---------------- epilogue ----------------
-    const int e = warp - 4, sp = e & 3, grp = e >> 2;
+    const int e = warp - 8, sp = e & 3, grp = e >> 2;
     const int row = sp * 32 + lane;                           // row within the CTA's 128
     const float alpha = __ldg(g.sa) * __ldg(g.sb);
-    unsigned char* stg = smem + OFF_STG + grp * 2 * STG_BYTES;
     const uint32_t tbase = tmem + ((uint32_t)(sp * 32) << 16) + grp * 128;
     int tc = 0;
     for (int t = pair; t < ntiles; t += npairs, ++tc) {
       int tm, tn;
       tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
-      mbar_wait(bar_accf, tc & 1);
+      mbar_wait_sleep(bar_accf, tc & 1);
       tc_fence_after();
-      uint32_t v[4][32];
+      const int gm = tm * PT + (int)rank * 128 + row, gn0 = tn * PT + grp * 128;
+      unsigned char* drow = static_cast<unsigned char*>(g.d) + (int64_t)gm * g.ldd * (F32 ? 4 : 2);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) Q2_LD32(v[q], tbase + q * 32);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_leader(bar_acce);            // MMA may overwrite the accumulator
-      const int gm0 = tm * PT + (int)rank * 128, gn0 = tn * PT + grp * 128;
-      constexpr int PASSES = F32 ? 2 : 1;                     // 32 KB of output per pass
+      for (int half = 0; half < 2; ++half) {                  // 64 columns per pass
+        uint32_t v[2][32];
+        Q2_LD32(v[0], tbase + half * 64);
+        Q2_LD32(v[1], tbase + half * 64 + 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (half == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(bar_acce);        // MMA may overwrite the accumulator
+        }
+        if (gm >= g.M) continue;
 #pragma unroll
-      for (int pass = 0; pass < PASSES; ++pass) {
-        if (lane == 0 && sp == 0 && (tc > 0 || pass > 0)) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        named_bar(1 + grp, 128);                              // staging free
+        for (int q = 0; q < 2; ++q) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {                         // box b of this pass: 128 rows x 128 B
-          unsigned char* base = stg + b * STG_BYTES + row * 128;
-          if (F32) {
-            const uint32_t* r = v[2 * pass + b];              // 32 fp32 columns
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-              *reinterpret_cast<float4*>(base + ((ch ^ (row & 7)) << 4)) =
-                  make_float4(alpha * __uint_as_float(r[4 * ch]), alpha * __uint_as_float(r[4 * ch + 1]),
-                              alpha * __uint_as_float(r[4 * ch + 2]), alpha * __uint_as_float(r[4 * ch + 3]));
-          } else {
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {                  // 64 bf16 columns: v[2b], v[2b+1]
-              const uint32_t* r = v[2 * b + (ch >> 2)] + 8 * (ch & 3);
+          for (int c8 = 0; c8 < 32; c8 += F32 ? 4 : 8) {
+            const int n = gn0 + 64 * half + 32 * q + c8;
+            if (F32) {
+              float4 o = make_float4(alpha * __uint_as_float(v[q][c8]), alpha * __uint_as_float(v[q][c8 + 1]),
+                                     alpha * __uint_as_float(v[q][c8 + 2]), alpha * __uint_as_float(v[q][c8 + 3]));
+              float* dp = reinterpret_cast<float*>(drow) + n;
+              if (n + 4 <= g.N) {
+                if (g.accumulate) { const float4 p = *reinterpret_cast<const float4*>(dp); o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w; }
+                *reinterpret_cast<float4*>(dp) = o;
+              } else {
+                const float oo[4] = {o.x, o.y, o.z, o.w};
+                for (int i = 0; i < 4 && n + i < g.N; ++i) dp[i] = g.accumulate ? dp[i] + oo[i] : oo[i];
+              }
+            } else {
               uint32_t p[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(r[2 * i]), alpha * __uint_as_float(r[2 * i + 1]));
+                __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(v[q][c8 + 2 * i]),
+                                                         alpha * __uint_as_float(v[q][c8 + 2 * i + 1]));
                 p[i] = *reinterpret_cast<uint32_t*>(&h);
               }
-              *reinterpret_cast<uint4*>(base + ((ch ^ (row & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+              __nv_bfloat16* dp = reinterpret_cast<__nv_bfloat16*>(drow) + n;
+              if (n + 8 <= g.N) {
+                *reinterpret_cast<uint4*>(dp) = make_uint4(p[0], p[1], p[2], p[3]);
+              } else {
+                for (int i = 0; i < 8 && n + i < g.N; ++i) dp[i] = reinterpret_cast<const __nv_bfloat16*>(p)[i];
+              }
             }
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_bar(1 + grp, 128);
-        if (lane == 0 && sp == 0) {
-          constexpr int BC = F32 ? 32 : 64;                   // columns per box
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-            tma_store_2d(&tmD, smem_u32(stg + b * STG_BYTES), gn0 + (2 * pass + b) * BC, gm0, g.accumulate != 0);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
       }
     }
-    if (lane == 0 && sp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -271,13 +318,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-static bool make_sf_map(CUtensorMap* map, const void* sf, int64_t R, int64_t K, uint32_t halves) {
+static bool make_sf_map(CUtensorMap* map, const void* sf, int64_t R, int64_t K, uint32_t halves, uint32_t groups_box) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   const uint64_t groups = (uint64_t)((R + 255) / 256) * (uint64_t)sf_kblocks(K) * 4;
   cuuint64_t dims[3] = {128, 2, (cuuint64_t)groups};
   cuuint64_t strides[2] = {128, 256};
-  cuuint32_t box[3] = {128, halves, 16};
+  cuuint32_t box[3] = {128, halves, groups_box};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(sf), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -298,7 +345,7 @@ static int launch_gemm(const CUtensorMap* maps, const GemmArgs& g, cudaStream_t 
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = g.tiles_m * g.tiles_n;
   const int npairs = std::max(1, std::min(ntiles, nsm / 2));
-  nvfp4_gemm_kernel<F32><<<2 * npairs, GEMM_THREADS, GEMM_SMEM, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], g);
+  nvfp4_gemm_kernel<F32><<<2 * npairs, GEMM_THREADS, GEMM_SMEM, st>>>(maps[0], maps[1], maps[2], maps[3], g);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
 }
@@ -315,14 +362,12 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
   const int esz = d_dtype == Q2_F32 ? 4 : 2;
   if (ldd < b->R || (ldd * esz) % 16 || (reinterpret_cast<uintptr_t>(d) & 15)) return Q2_EINVAL;
   if (a->R > INT32_MAX || b->R > INT32_MAX || a->K > INT32_MAX) return Q2_EINVAL;
-  CUtensorMap maps[5];
+  CUtensorMap maps[4];
   if (!make_map(&maps[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, a->codes, a->K / 2, a->R, a->K / 2, BKB, 128) ||
       !make_map(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, b->codes, b->K / 2, b->R, b->K / 2, BKB, 128) ||
-      !make_sf_map(&maps[2], a->sf, a->R, a->K, 1) || !make_sf_map(&maps[3], b->sf, b->R, b->K, 2) ||
-      !make_map(&maps[4], d_dtype == Q2_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d,
-                b->R, a->R, ldd * esz, d_dtype == Q2_F32 ? 32 : 64, 128))
+      !make_sf_map(&maps[2], a->sf, a->R, a->K, 1, 16) || !make_sf_map(&maps[3], b->sf, b->R, b->K, 2, 16))
     return Q2_ECUDA;
-  GemmArgs g{a->scale32, b->scale32, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
+  GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
              (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
