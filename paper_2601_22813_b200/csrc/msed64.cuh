@@ -395,13 +395,11 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
 
     // ------------------------------------------------------- group maxima
-    // fp32 truncations rz(y) feed the codes and the group maxima: max |rz(y)| =
-    // rz(max |y|) (rz is monotone), so gmax lies in [gmf, nextup(gmf)).
+    // From the float64 high words: gmax lies in [H 2^32, (H+1) 2^32) for the
+    // largest |y| high word H of the group; the scale is certified on that
+    // bracket below (ties in the low word cannot change a certified scale).
     const bool live = r < a.R;
-    float yf[16][2];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) { yf[k][0] = __double2float_rz(y[k][0]); yf[k][1] = __double2float_rz(y[k][1]); }
-#define YF(k, b) yf[k][b]
+#define YF(k, b) __double2float_rz(y[k][b])
     if (MODE == M64_ABSMAX || MODE == M64_PMAX || (MODE == M64_POSTHOC && a.pseudo)) {
       // exact |x_rot| max (exact-mode scale32 / pass-1 API reduction)
       uint64_t m = 0;
@@ -411,33 +409,48 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       if (live) wabs = umax64(wabs, m);
       if (MODE == M64_ABSMAX) continue;
     }
-    float gv[8];
+    uint32_t gv[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g)
-      gv[g] = fmaxf(fmaxf(fabsf(YF(2 * g, 0)), fabsf(YF(2 * g, 1))), fmaxf(fabsf(YF(2 * g + 1, 0)), fabsf(YF(2 * g + 1, 1))));
+    for (int g = 0; g < 8; ++g) {
+      const uint32_t M = 0x7FFFFFFFu;
+      gv[g] = max(max((uint32_t)(dbits(y[2 * g][0]) >> 32) & M, (uint32_t)(dbits(y[2 * g][1]) >> 32) & M),
+                  max((uint32_t)(dbits(y[2 * g + 1][0]) >> 32) & M, (uint32_t)(dbits(y[2 * g + 1][1]) >> 32) & M));
+    }
     // reduce-scatter over the quad: lane q ends with groups 2q, 2q+1
-    float w4[4], gq[2];
+    uint32_t w4[4], gqh[2];
     {
       const bool hi2 = q & 2, hi1 = q & 1;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float snd = hi2 ? gv[i] : gv[4 + i], keep = hi2 ? gv[4 + i] : gv[i];
-        w4[i] = fmaxf(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 2));
+        const uint32_t snd = hi2 ? gv[i] : gv[4 + i], keep = hi2 ? gv[4 + i] : gv[i];
+        w4[i] = max(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 2));
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const float snd = hi1 ? w4[i] : w4[2 + i], keep = hi1 ? w4[2 + i] : w4[i];
-        gq[i] = fmaxf(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 1));
+        const uint32_t snd = hi1 ? w4[i] : w4[2 + i], keep = hi1 ? w4[2 + i] : w4[i];
+        gqh[i] = max(keep, __shfl_xor_sync(0xFFFFFFFFu, snd, 1));
       }
     }
-    // ------------------------------------------------------ group scales d
-    // certified from the bracket [gmf, nextup(gmf)) with directed fp32 rounding;
-    // a warp with any uncertain group recomputes its scales from exact maxima.
-    uint32_t dkey[2];                                 // posthoc: d as fp32 bits; quant: s8
-    bool unc = false;
+    // fp32 bracket [glo, gup] of gmax from the high word (fp32-normal range only)
+    float gq[2], gqu[2];
+    bool rng_bad = false;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const float glo = gq[j], gup = __uint_as_float(__float_as_uint(gq[j]) + 1u);
+      const uint32_t H = gqh[j], e11 = H >> 20;
+      const bool ok = e11 >= 897u && e11 <= 1149u;
+      const uint32_t fb = ((H - (896u << 20)) << 3);
+      gq[j] = ok ? __uint_as_float(fb) : 0.f;
+      gqu[j] = ok ? __uint_as_float(fb + 8u) : 0.f;
+      rng_bad |= !ok && H != 0u;                          // zero groups are exact (gmax = 0)
+    }
+    // ------------------------------------------------------ group scales d
+    // certified from the bracket [glo, gup] with directed fp32 rounding; a warp
+    // with any uncertain group recomputes its scales from exact float64 maxima.
+    uint32_t dkey[2];                                 // posthoc: d as fp32 bits; quant: s8
+    bool unc = rng_bad;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float glo = gq[j], gup = gqu[j];
       if (MODE == M64_QUANT) {
         const float lo = __fmul_rd(glo, isd_lo), hi = __fmul_ru(gup, isd_hi);
         uint32_t cl, ch;
@@ -450,7 +463,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         const float lo = __fmul_rd(glo, is_lo), hi = __fmul_ru(gup, is_hi);
         const uint32_t pl = rne4(lo), ph = rne4(hi);
         dkey[j] = pl;
-        unc |= pl != ph || !(lo >= 0x1p-125f) || !(hi < 0x1p126f);
+        unc |= gqh[j] != 0u && (pl != ph || !(lo >= 0x1p-125f) || !(hi < 0x1p126f));   // gmax = 0: pseudo 0
       }
     }
     if (__any_sync(0xFFFFFFFFu, unc)) {
