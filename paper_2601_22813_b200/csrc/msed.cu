@@ -139,9 +139,9 @@ static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 using namespace q2;
 
-// ws: red (256 B) | per-group SR words u16 [R, K/16]
+// ws: red (256 B) | pseudo-scales bf16 [R, K/16] | EDEN factors f64 [R, K/128]
 extern "C" size_t q2_msed_ws_bytes(int64_t R, int64_t K) {
-  return 256 + align256((size_t)R * (K / 16) * 2);
+  return 256 + align256((size_t)R * (K / 16) * 2) + align256((size_t)R * (K / 128) * 8);
 }
 
 extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R,
@@ -162,11 +162,12 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   a.sr_head = prng_head(seed_sr, sr_stream);
   if (cudaMemsetAsync(w, 0, 16, st) != cudaSuccess) return Q2_ECUDA;
   if (mode == Q2_MSED_POSTHOC) {
-    a.aword = reinterpret_cast<uint16_t*>(w + 256);
+    a.pseudo = reinterpret_cast<uint16_t*>(w + 256);
+    a.corr = reinterpret_cast<double*>(w + 256 + align256((size_t)R * (K / 16) * 2));
     if ((rc = dispatch_m64<M64_POSTHOC>(src, a, st))) return rc;
     const int64_t quads = R * (K / 64);
     msed64_pass2_kernel<<<(unsigned)std::max<int64_t>(1, (quads + 255) / 256), 256, 0, st>>>(
-        a.aword, a.red, R, K, out->sf, out->scale32, err);
+        a.pseudo, a.corr, a.red, R, K, a.sr_head, out->sf, out->scale32, err);
     Q2_CHECK_LAUNCH();
     return Q2_OK;
   }
@@ -190,7 +191,7 @@ extern "C" int q2_posthoc_pass1(const void* x, int dtype, const q2_nvfp4* tape, 
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   M64Args a = base_args(src, R, K, sign_mask, s, inv_sqrt_chunk);
-  a.codes = codes; a.pseudo = pseudo_bf16; a.corr = corr;
+  a.codes = codes; a.pseudo = pseudo_bf16; a.corr = corr; a.want_absmax = 1;
   a.red = reinterpret_cast<unsigned long long*>(red); a.err = err;
   if (cudaMemsetAsync(red, 0, 16, st) != cudaSuccess) return Q2_ECUDA;
   return dispatch_m64<M64_POSTHOC>(src, a, st);

@@ -48,8 +48,8 @@ struct M64Args {
   uint64_t sr_head;
   int pow2;                                       // M64_QUANT: scale32 = 2^k from red[1]
   uint8_t* codes; uint8_t* sf; float* scale32;
-  uint16_t* aword;                                // posthoc: per-group SR word (see pack_aword)
-  uint16_t* pseudo; double* corr;                 // optional posthoc pass-1 API outputs
+  uint16_t* pseudo; double* corr;                 // posthoc pass-1 outputs (pass 2 inputs)
+  int want_absmax;                                // posthoc: also reduce the exact |x_rot| max (API pass1)
   unsigned long long* red;                        // [0] |x_rot| max, [1] pseudo max (f64 bits)
   uint32_t* err;
   int tiles_r, tiles_c;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     // bracket below (ties in the low word cannot change a certified scale).
     const bool live = r < a.R;
 #define YF(k, b) __double2float_rz(y[k][b])
-    if (MODE == M64_ABSMAX || MODE == M64_PMAX || (MODE == M64_POSTHOC && a.pseudo)) {
+    if (MODE == M64_ABSMAX || MODE == M64_PMAX || (MODE == M64_POSTHOC && a.want_absmax)) {
       // exact |x_rot| max (exact-mode scale32 / pass-1 API reduction)
       uint64_t m = 0;
 #pragma unroll
@@ -612,30 +612,27 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     __syncwarp();
     const uint4 cw4 = *reinterpret_cast<const uint4*>(cst + rw * 80 + 16 * q);
     __syncwarp();
-    // per-group scale outputs: lane q owns groups 2q, 2q+1
+    // per-group scale outputs: lane q owns groups 2q, 2q+1.  Post-hoc mode hands
+    // (pseudo, S) to pass 2, which runs the per-group PRNG and SR at full occupancy.
     const int64_t g0 = r * gpr + (int64_t)tc * 8 + 2 * q;
-    uint32_t wv[2];
+    uint32_t wv[2] = {0u, 0u};
+    if (MODE == M64_QUANT) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t z = mix64(a.sr_head ^ ((uint64_t)(g0 + j) + GOLDEN));
-      const double dj = MODE == M64_QUANT ? e4m3_val(dkey[j]) : (double)__uint_as_float(dkey[j]);
-      if (MODE == M64_POSTHOC) {
-        wv[j] = pack_aword(__dmul_rn(S, dj), z >> 11);
-      } else {
+      for (int j = 0; j < 2; ++j) {
+        const uint64_t z = mix64(a.sr_head ^ ((uint64_t)(g0 + j) + GOLDEN));
         bool o2 = false;
-        wv[j] = zero ? 0u : sr_code_direct(__dmul_rn(S, dj), z >> 11, &o2);
+        wv[j] = zero ? 0u : sr_code_direct(__dmul_rn(S, e4m3_val(dkey[j])), z >> 11, &o2);
         if (live && o2) ovf = true;
       }
     }
     const uint32_t half = wv[0] | (wv[1] << 8);
-    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, half, 1);
+    const uint32_t other = MODE == M64_QUANT ? __shfl_xor_sync(0xFFFFFFFFu, half, 1) : 0u;
     if (live) {
       *reinterpret_cast<uint4*>(a.codes + r * (a.K / 2) + (int64_t)tc * 64 + 16 * q) = cw4;
       if (MODE == M64_POSTHOC) {
         wp = umax64(wp, dbits((double)__uint_as_float(max(dkey[0], dkey[1]))));
-        if (a.aword) *reinterpret_cast<uint32_t*>(a.aword + g0) = wv[0] | (wv[1] << 16);
-        if (a.pseudo) *reinterpret_cast<uint32_t*>(a.pseudo + g0) = (dkey[0] >> 16) | (dkey[1] & 0xFFFF0000u);
-        if (a.corr && q == 0) a.corr[r * (a.K / CHUNK) + tc] = S;
+        *reinterpret_cast<uint32_t*>(a.pseudo + g0) = (dkey[0] >> 16) | (dkey[1] & 0xFFFF0000u);
+        if (q == 0) a.corr[r * (a.K / CHUNK) + tc] = S;
       } else if ((q & 1) == 0) {                      // lanes 2m: the 4-scale word of groups 4m..4m+3
         const uint32_t word = half | (other << 16);
         *reinterpret_cast<uint32_t*>(a.sf + sf_offset(r, (int64_t)tc * 8 + 2 * q, sf_kblocks(a.K))) = word;
@@ -659,11 +656,14 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   if (nanscale) atomic_or_err(a.err, Q2_ERR_NAN_SCALE);
 }
 
-// Post-hoc pass 2 (posthoc.py:98-125): k from the pseudo-scale max, then each
-// group's E4M3 code from its pass-1 SR word.  One thread per 4 groups.
-__global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __restrict__ aword,
+// Post-hoc pass 2 (posthoc.py:98-125): k from the pseudo-scale max, then per
+// group v = fl64(S * pseudo) (exact: pseudo has 4 significant bits), its E4M3
+// truncation a and the SR decision u < p (both invariant under the 2^-k shift,
+// pack_aword), and the shifted code (aword_code).  One thread per 4 groups.
+__global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __restrict__ pseudo,
+                                                           const double* __restrict__ corr,
                                                            const unsigned long long* __restrict__ red, int64_t R,
-                                                           int64_t K, uint8_t* __restrict__ sf,
+                                                           int64_t K, uint64_t sr_head, uint8_t* __restrict__ sf,
                                                            float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
   const int64_t qpr = K / 64, total = R * qpr;
   const double pmax = __longlong_as_double((long long)red[1]);
@@ -673,16 +673,22 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
   if (tq == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
   if (tq >= total) return;
   const int64_t r = tq / qpr, jq = tq - r * qpr;
-  uint32_t* dst = reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, sf_kblocks(K)));
   uint32_t word = 0;
   bool ovf = false;
   if (pmax > 0.0) {
-    const uint2 w = *reinterpret_cast<const uint2*>(aword + r * (K / GROUP) + 4 * jq);
-    word = aword_code(w.x & 0xFFFF, k, &ovf) | (aword_code(w.x >> 16, k, &ovf) << 8) |
-           (aword_code(w.y & 0xFFFF, k, &ovf) << 16) | (aword_code(w.y >> 16, k, &ovf) << 24);
+    const int64_t g0 = r * (K / GROUP) + 4 * jq;
+    const uint2 pw = *reinterpret_cast<const uint2*>(pseudo + g0);
+    const double S = corr[r * (K / CHUNK) + (jq >> 1)];
+    const uint32_t ps[4] = {pw.x << 16, pw.x & 0xFFFF0000u, pw.y << 16, pw.y & 0xFFFF0000u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t z = mix64(sr_head ^ ((uint64_t)(g0 + i) + GOLDEN));
+      const uint32_t w = pack_aword(__dmul_rn(S, (double)__uint_as_float(ps[i])), z >> 11);
+      word |= aword_code(w, k, &ovf) << (8 * i);
+    }
   }
   if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
-  *dst = word;
+  *reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, sf_kblocks(K))) = word;
 }
 
 }  // namespace q2
