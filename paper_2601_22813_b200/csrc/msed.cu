@@ -166,8 +166,10 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
     a.corr = reinterpret_cast<double*>(w + 256 + align256((size_t)R * (K / 16) * 2));
     if ((rc = dispatch_m64<M64_POSTHOC>(src, a, st))) return rc;
     const int64_t quads = R * (K / 64);
+    if (quads >= (1ll << 31)) return Q2_EINVAL;
     msed64_pass2_kernel<<<(unsigned)std::max<int64_t>(1, (quads + 255) / 256), 256, 0, st>>>(
-        a.pseudo, a.corr, a.red, R, K, a.sr_head, out->sf, out->scale32, err);
+        a.pseudo, a.corr, a.red, (uint32_t)R, (uint32_t)K, FastDiv((uint32_t)(K / 64)), a.sr_head, out->sf,
+        out->scale32, err);
     Q2_CHECK_LAUNCH();
     return Q2_OK;
   }

@@ -662,21 +662,22 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
 // pack_aword), and the shifted code (aword_code).  One thread per 4 groups.
 __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __restrict__ pseudo,
                                                            const double* __restrict__ corr,
-                                                           const unsigned long long* __restrict__ red, int64_t R,
-                                                           int64_t K, uint64_t sr_head, uint8_t* __restrict__ sf,
-                                                           float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
-  const int64_t qpr = K / 64, total = R * qpr;
+                                                           const unsigned long long* __restrict__ red, uint32_t R,
+                                                           uint32_t K, FastDiv fq, uint64_t sr_head,
+                                                           uint8_t* __restrict__ sf, float* __restrict__ scale32_out,
+                                                           uint32_t* __restrict__ err) {
+  const uint32_t qpr = K / 64, total = R * qpr;       // quads of 4 groups (< 2^26 for any tensor here)
   const double pmax = __longlong_as_double((long long)red[1]);
   int k = 0;
   if (pmax > 0.0) { int e; const double m = frexp(pmax / 256.0, &e); k = (m == 0.5) ? e - 1 : e; }
-  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t tq = blockIdx.x * blockDim.x + threadIdx.x;
   if (tq == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
   if (tq >= total) return;
-  const int64_t r = tq / qpr, jq = tq - r * qpr;
+  const uint32_t r = fq.div(tq), jq = tq - r * qpr;
   uint32_t word = 0;
   bool ovf = false;
   if (pmax > 0.0) {
-    const int64_t g0 = r * (K / GROUP) + 4 * jq;
+    const uint32_t g0 = r * (K / GROUP) + 4 * jq;
     const uint2 pw = *reinterpret_cast<const uint2*>(pseudo + g0);
     const double S = corr[r * (K / CHUNK) + (jq >> 1)];
     const uint32_t ps[4] = {pw.x << 16, pw.x & 0xFFFF0000u, pw.y << 16, pw.y & 0xFFFF0000u};
