@@ -667,9 +667,12 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
                                                            uint8_t* __restrict__ sf, float* __restrict__ scale32_out,
                                                            uint32_t* __restrict__ err) {
   const uint32_t qpr = K / 64, total = R * qpr;       // quads of 4 groups (< 2^26 for any tensor here)
-  const double pmax = __longlong_as_double((long long)red[1]);
-  int k = 0;
-  if (pmax > 0.0) { int e; const double m = frexp(pmax / 256.0, &e); k = (m == 0.5) ? e - 1 : e; }
+  // k = smallest integer with pmax / 2^k <= 256 (ms_eden.py:86-91); pmax is 0 or a
+  // normal E8M3 value, so k = E - 8 for a power of two and E - 7 otherwise
+  const uint64_t pb = red[1];
+  const double pmax = __longlong_as_double((long long)pb);
+  const int E = (int)(pb >> 52) - 1023;
+  const int k = (pb & ((1ull << 52) - 1)) == 0 ? E - 8 : E - 7;
   const uint32_t tq = blockIdx.x * blockDim.x + threadIdx.x;
   if (tq == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
   if (tq >= total) return;
@@ -683,9 +686,17 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
     const uint32_t ps[4] = {pw.x << 16, pw.x & 0xFFFF0000u, pw.y << 16, pw.y & 0xFFFF0000u};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint64_t z = mix64(sr_head ^ ((uint64_t)(g0 + i) + GOLDEN));
-      const uint32_t w = pack_aword(__dmul_rn(S, (double)__uint_as_float(ps[i])), z >> 11);
-      word |= aword_code(w, k, &ovf) << (8 * i);
+      const uint64_t u53 = mix64(sr_head ^ ((uint64_t)(g0 + i) + GOLDEN)) >> 11;
+      const uint64_t b = dbits(__dmul_rn(S, (double)__uint_as_float(ps[i])));
+      const int Ex = (int)(b >> 52) - 1023 - k;           // binade of the shifted scale x = v 2^-k
+      uint32_t code;
+      if (Ex >= -6 && Ex < 8) {                           // E4M3-normal, below 256: SR on the mantissa
+        const uint64_t low49 = b & ((1ull << 49) - 1);
+        code = ((uint32_t)(Ex + 7) << 3) + (uint32_t)((b >> 49) & 7) + (u53 < (low49 << 4) ? 1u : 0u);
+      } else {
+        code = aword_code(pack_aword(bitsd(b), u53), k, &ovf);
+      }
+      word |= code << (8 * i);
     }
   }
   if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
