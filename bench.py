@@ -52,7 +52,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -137,7 +137,7 @@ def cpu_baseline_sample(mode: str) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="posthoc", choices=["posthoc", "exact"])
@@ -340,14 +340,21 @@ def kernel_breakdown(q2, data, cfg, dev):
         kernels[tag] = {"ms": t, "launches": len(lst), ("TFLOP/s" if unit == "F" else "GB/s"): rate}
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     d = kernels[dom]
+    # DRAM bytes per algorithmic byte from `ncu --set full` captures (profiles/round1_summary.md)
+    measured_ratio = {"msed_cols_bf16": 475.4 / 472.8, "msed_rows_bf16": 475.4 / 472.8}
+    launches = d["launches"]
+    work_per_launch = sum(x[2] for x in acc[dom]) / launches
     if "TFLOP/s" in d:
         peak = 4.0 * bf16
         roof = {"bound": "tensor", "kernel": dom, "achieved": d["TFLOP/s"], "peak": peak, "unit": "TFLOP/s",
                 "frac": d["TFLOP/s"] / peak, "traffic": None,
                 "peak_source": f"4 x bf16_tflops of {src} (dense NVFP4:BF16 = 4:1 on B200)"}
     else:
+        traffic = work_per_launch * measured_ratio[dom] if dom in measured_ratio else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": d["GB/s"], "peak": hbm, "unit": "GB/s",
-                "frac": d["GB/s"] / hbm, "traffic": None, "peak_source": f"hbm_gbs of {src}"}
+                "frac": d["GB/s"] / hbm, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram r+w)",
+                "algorithmic_bytes_per_launch": work_per_launch, "peak_source": f"hbm_gbs of {src}",
+                "note": "compute-bound: literal float64 MS-EDEN (DESIGN.md §5)"}
     total = sum(k["ms"] for k in kernels.values())
     for k in kernels.values():
         k["share"] = k["ms"] / total
