@@ -90,7 +90,7 @@ static int launch_m64(const M64Src& s, const M64Args& a, cudaStream_t st) {
   bool ok;
   if (SRC == Q2_SRC_TAPE_COLS) {
     ok = make_map(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, s.tape->codes, (uint64_t)(a.R / 2), (uint64_t)a.K,
-                  (uint64_t)(a.R / 2), 32, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+                  (uint64_t)(a.R / 2), 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
   } else {
     const CUtensorMapDataType dt = DT == Q2_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const int esz = DT == Q2_BF16 ? 2 : 4, bi = DT == Q2_BF16 ? 64 : 32;

@@ -36,9 +36,9 @@
 namespace q2 {
 
 enum { M64_ABSMAX = 0, M64_PMAX = 1, M64_QUANT = 2, M64_POSTHOC = 3 };
-constexpr int M64_ROWS = 64;                      // logical rows per tile
-constexpr int M64_CONSUMERS = 256;
-constexpr int M64_THREADS = M64_CONSUMERS + 32;
+constexpr int M64_ROWS = 128;                     // logical rows per tile (16 warps x 8)
+constexpr int M64_WARPS = 16;
+constexpr int M64_THREADS = 32 * M64_WARPS;
 
 struct M64Args {
   const uint8_t* tape_sf; const float* tape_scale32;
@@ -57,12 +57,12 @@ struct M64Args {
 
 template <int SRC, int DT>
 struct M64Tile {
-  static constexpr int RAW = SRC == Q2_SRC_TAPE_COLS ? 4096 + 1024 : (DT == Q2_BF16 ? 16384 : 32768);
+  static constexpr int RAW = SRC == Q2_SRC_TAPE_COLS ? 8192 + 2048 : (DT == Q2_BF16 ? 32768 : 65536);
   static constexpr int STAGES = SRC == Q2_SRC_TAPE_COLS ? 6 : (DT == Q2_BF16 ? 4 : 3);
-  static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? 2 * 16384 : 0;     // decoded f16 tiles
+  static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? 2 * 32768 : 0;     // decoded f16 tiles
   static constexpr int OFF_DEC = STAGES * RAW;
-  static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 8 x 640 B
-  static constexpr int OFF_SGN = OFF_CST + 8 * 640;                      // 4 x 16 sign words
+  static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 16 x 640 B
+  static constexpr int OFF_SGN = OFF_CST + M64_WARPS * 640;              // 4 x 16 sign words
   static constexpr int OFF_BAR = OFF_SGN + 256;
   static constexpr int SMEM = OFF_BAR + 128 + 1024;
 };
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < TL::STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
-      mbar_init(bar_empty + 8 * s, SRC == Q2_SRC_TAPE_COLS ? M64_CONSUMERS / 32 : 8);
+      mbar_init(bar_empty + 8 * s, M64_WARPS);
     }
     mbar_fence_init();
   }
@@ -193,31 +193,34 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   }
   __syncthreads();
 
-  if (warp == 8) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-      const int64_t kb = sf_kblocks(a.R);
-      int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
-        const int s = it % TL::STAGES;
-        if (it >= TL::STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / TL::STAGES) - 1) & 1);
-        const uint32_t dst = smem_u32(smem + s * TL::RAW), fb = bar_full + 8 * s;
-        mbar_expect_tx(fb, TL::RAW);
-        if (SRC == Q2_SRC_ROWS) {
-          const int nb = DT == Q2_BF16 ? 2 : 4, w = DT == Q2_BF16 ? 64 : 32;
-          for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 8192, &tm, tc * CHUNK + j * w, tr * M64_ROWS, fb);
-        } else if (SRC == Q2_SRC_COLS) {
-          const int nb = DT == Q2_BF16 ? 1 : 2;
-          for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 16384, &tm, tr * M64_ROWS + j * 32, tc * CHUNK, fb);
-        } else {
-          tma_load_2d(dst, &tm, tr * 32, tc * CHUNK, fb);                  // codes [128 tape rows x 32 B]
-          bulk_load(dst + 4096, a.tape_sf + ((((int64_t)tc >> 1) * kb + tr) << 10), 1024, fb);
-        }
-      }
+  // ---------------------------------------------------------- TMA producer
+  // Thread 0 refills the ring: tile i goes to stage i % STAGES once all warps
+  // released that stage's previous tile (they do so right after reading it).
+  const int64_t sf_kb = sf_kblocks(a.R);
+  auto issue = [&](int i) {
+    const int t = blockIdx.x + i * gridDim.x;
+    if (t >= ntiles) return;
+    const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
+    const int s = i % TL::STAGES;
+    if (i >= TL::STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((i / TL::STAGES) - 1) & 1);
+    const uint32_t dst = smem_u32(smem + s * TL::RAW), fb = bar_full + 8 * s;
+    // tape: the second 1 KiB scale block does not exist when R % 128 == 64
+    const int sfb = SRC == Q2_SRC_TAPE_COLS ? (2 * tr + 1 < sf_kb ? 2048 : 1024) : 0;
+    mbar_expect_tx(fb, SRC == Q2_SRC_TAPE_COLS ? 8192 + sfb : TL::RAW);
+    if (SRC == Q2_SRC_ROWS) {
+      const int nb = DT == Q2_BF16 ? 2 : 4, w = DT == Q2_BF16 ? 64 : 32;
+      for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 16384, &tm, tc * CHUNK + j * w, tr * M64_ROWS, fb);
+    } else if (SRC == Q2_SRC_COLS) {
+      const int nb = DT == Q2_BF16 ? 2 : 4, w = DT == Q2_BF16 ? 64 : 32;
+      for (int j = 0; j < nb; ++j) tma_load_2d(dst + j * 16384, &tm, tr * M64_ROWS + j * w, tc * CHUNK, fb);
+    } else {
+      tma_load_2d(dst, &tm, tr * 64, tc * CHUNK, fb);                        // codes [128 tape rows x 64 B]
+      bulk_load(dst + 8192, a.tape_sf + ((((int64_t)tc >> 1) * sf_kb + 2 * tr) << 10), sfb, fb);
     }
-    return;
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+    for (int i = 0; i < TL::STAGES - 1; ++i) issue(i);
   }
 
   // -------------------------------------------------------------- consumers
@@ -257,26 +260,29 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
     const int s = it % TL::STAGES;
+    if (threadIdx.x == 0) issue(it + TL::STAGES - 1);
     mbar_wait_sleep(bar_full + 8 * s, (it / TL::STAGES) & 1);
     const uint32_t st = smem_u32(smem + s * TL::RAW);
     const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
     double y[16][2];
 
     if (SRC == Q2_SRC_TAPE_COLS) {
-      // decode the NVFP4 tape block [128 tape rows x 64 tape cols] into f16 (exact:
-      // FP4*E4M3 has <= 6 significant bits), random sign of the tape row applied
-      unsigned char* dec = smem + TL::OFF_DEC + (it & 1) * 16384;
+      // decode the NVFP4 tape block [128 tape rows x 128 tape cols] into f16 (exact:
+      // FP4*E4M3 has <= 6 significant bits), random sign of the tape row applied.
+      // dec: two 64-column halves of [128 rows x 128 B], 16-B segments XOR-swizzled.
+      unsigned char* dec = smem + TL::OFF_DEC + (it & 1) * 32768;
       {
-        const int tri = threadIdx.x & 127, h = threadIdx.x >> 7;
-        const uint4 cw = *reinterpret_cast<const uint4*>(smem + s * TL::RAW + tri * 32 + h * 16);
+        const int tri = threadIdx.x & 127, h = threadIdx.x >> 7;               // tape row, 32-column quarter
+        const uint4 cw = *reinterpret_cast<const uint4*>(smem + s * TL::RAW + tri * 64 + h * 16);
         const int L = tri & 31;
-        const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + s * TL::RAW + 4096 + ((L >> 3) << 8) +
-                                                                ((tc & 1) << 7) + ((L & 7) << 4) + ((tri >> 5) << 2));
+        const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + s * TL::RAW + 8192 + (h >> 1) * 1024 +
+                                                                ((L >> 3) << 8) + ((tc & 1) << 7) + ((L & 7) << 4) +
+                                                                ((tri >> 5) << 2));
         const uint32_t neg = ((a.sign[tri >> 5] >> (tri & 31)) & 1u) ? 0x80008000u : 0u;
         uint32_t sc[2];
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          const uint32_t s8 = (sfw >> (8 * (2 * h + g))) & 0xFF;
+          const uint32_t s8 = (sfw >> (8 * (2 * (h & 1) + g))) & 0xFF;
           asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(sc[g]) : "h"((unsigned short)(s8 | (s8 << 8))));
         }
         const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
@@ -291,18 +297,18 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          *reinterpret_cast<uint4*>(dec + tri * 128 + (((4 * h + j) ^ (tri & 7)) << 4)) =
+          *reinterpret_cast<uint4*>(dec + (h >> 1) * 16384 + tri * 128 + (((4 * (h & 1) + j) ^ (tri & 7)) << 4)) =
               make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + 8 * s);
-      named_bar(1, M64_CONSUMERS);
+      named_bar(1, M64_THREADS);
       const uint32_t db = smem_u32(dec);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t v[4];
         const int k = 4 * i + (lane >> 3), ri = lane & 7;
-        ldsm_x4_t(db + (8 * k + ri) * 128 + ((warp ^ ri) << 4), v);
+        ldsm_x4_t(db + (warp >> 3) * 16384 + (8 * k + ri) * 128 + (((warp & 7) ^ ri) << 4), v);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float f0, f1;
@@ -318,9 +324,9 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         uint32_t v[4];
         const int k = 4 * i + (lane >> 3), ri = lane & 7;
         if (SRC == Q2_SRC_ROWS)
-          ldsm_x4(st + (k >> 3) * 8192 + (8 * warp + ri) * 128 + (((k & 7) ^ ri) << 4), v);
+          ldsm_x4(st + (k >> 3) * 16384 + (8 * warp + ri) * 128 + (((k & 7) ^ ri) << 4), v);
         else
-          ldsm_x4_t(st + (8 * k + ri) * 128 + ((warp ^ ri) << 4), v);
+          ldsm_x4_t(st + (warp >> 3) * 16384 + (8 * k + ri) * 128 + (((warp & 7) ^ ri) << 4), v);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           // bf16 -> float64 * 2^-896 by moving the fields (exact, zeros and subnormals
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           float f;
           if (SRC == Q2_SRC_ROWS) {
             const int row = 8 * warp + rw;
-            f = *reinterpret_cast<const float*>(tile + (e >> 5) * 8192 + row * 128 + ((((e & 31) >> 2) ^ (row & 7)) << 4) + (e & 3) * 4);
+            f = *reinterpret_cast<const float*>(tile + (e >> 5) * 16384 + row * 128 + ((((e & 31) >> 2) ^ (row & 7)) << 4) + (e & 3) * 4);
           } else {
             const int col = 8 * warp + rw;
             f = *reinterpret_cast<const float*>(tile + (col >> 5) * 16384 + e * 128 + ((((col & 31) >> 2) ^ (e & 7)) << 4) + (col & 3) * 4);
