@@ -33,16 +33,13 @@ __device__ __forceinline__ void sf_store(uint8_t* sf, int64_t r, int64_t j, int6
 }
 
 // ------------------------------------------------------------------ E2M1 ----
-// magnitude code -> value (formats.py:43-46); code 8 is +0.
+// code -> value (formats.py:43-46) by bit construction (no local-memory table):
+// |value| = 2^((m>>1)-1) * (1 or 1.5); code 8 decodes to +0.
 __device__ __forceinline__ double fp4_val(uint32_t code) {
-  const double mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
-  double v = mag[code & 7];
-  return (code & 8) ? -v : v;
-}
-__device__ __forceinline__ float fp4_valf(uint32_t code) {
-  const float mag[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
-  float v = mag[code & 7];
-  return (code & 8) ? -v : v;
+  const uint32_t m = code & 7u;
+  uint32_t hi = m <= 1u ? (m ? 0x3FE00000u : 0u) : (((0x3FEu + (m >> 1)) << 20) | ((m & 1u) << 19));
+  hi |= m ? (code & 8u) << 28 : 0u;
+  return __longlong_as_double((long long)((uint64_t)hi << 32));
 }
 
 // ------------------------------------------------------------------ E4M3 ----
