@@ -612,11 +612,14 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
 
     // ----------------------------------------------------------- outputs
     // codes: byte k of this lane is chunk byte 4k + q; stage through smem (80 B row pitch)
-    unsigned char* cst = smem + TL::OFF_CST + warp * 640;
+    const uint32_t cst = smem_u32(smem + TL::OFF_CST + warp * 640) + rw * 80;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) cst[rw * 80 + 4 * k + q] = (unsigned char)(cw[k >> 2] >> (8 * (k & 3)));
+    for (int k = 0; k < 16; ++k)
+      asm volatile("st.shared.u8 [%0], %1;" ::"r"(cst + 4 * k + q), "r"(cw[k >> 2] >> (8 * (k & 3))) : "memory");
     __syncwarp();
-    const uint4 cw4 = *reinterpret_cast<const uint4*>(cst + rw * 80 + 16 * q);
+    uint4 cw4;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(cw4.x), "=r"(cw4.y), "=r"(cw4.z), "=r"(cw4.w)
+                 : "r"(cst + 16 * q) : "memory");
     __syncwarp();
     // per-group scale outputs: lane q owns groups 2q, 2q+1.  Post-hoc mode hands
     // (pseudo, S) to pass 2, which runs the per-group PRNG and SR at full occupancy.
