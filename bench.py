@@ -211,7 +211,7 @@ def main():
     # all-reduce; host-side Python/ctypes launch overhead removed).  Seeds are
     # baked into the captured launches, which does not change the work done.
     graph, launch = None, "eager"
-    if not args.eager:
+    if not args.eager and world == 1:      # N > 1: eager launches (no NCCL inside a captured graph)
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
