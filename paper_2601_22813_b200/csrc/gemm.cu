@@ -34,6 +34,8 @@
 //            16-byte vectors straight to global (read-add-write when accumulating).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cstdio>
+#include <cstdlib>
 #include "tc_common.cuh"
 
 namespace q2 {
@@ -63,7 +65,13 @@ struct GemmArgs {
   int M, N, K, kb;                                        // kb = ceil(K/64) scale blocks per row block
   int tiles_m, tiles_n, nk;
   int accumulate;
+  unsigned long long* trace;                              // optional timeline probe (pair 0), else nullptr
 };
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -113,6 +121,22 @@ __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
 // scale-factor source descriptor: core matrices of 8 lanes x 16 B, `sbo` bytes apart
 __device__ __forceinline__ uint64_t desc_sf32(uint32_t saddr, uint32_t sbo) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void tmem_ld64(uint32_t* r, uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,"
+      "%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+        "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+        "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+        "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+        "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
 }
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
@@ -198,6 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       for (int t = pair; t < ntiles; t += npairs, ++tc) {
         if (tc >= 1) mbar_wait(bar_acce, (tc - 1) & 1);       // both epilogues drained the accumulator
         tc_fence_after();
+        if (g.trace && pair == 0 && tc < 64) g.trace[4 * tc] = gtime();
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
           mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
@@ -215,6 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tc2_commit(bar_empty + 8 * s);
         }
         tc2_commit(bar_accf);
+        if (g.trace && pair == 0 && tc < 64) g.trace[4 * tc + 1] = gtime();
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -260,18 +286,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
       mbar_wait_sleep(bar_accf, tc & 1);
       tc_fence_after();
+      if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 2] = gtime();
       const int gm = tm * PT + (int)rank * 128 + row, gn0 = tn * PT + grp * 128;
       unsigned char* drow = static_cast<unsigned char*>(g.d) + (int64_t)gm * g.ldd * (F32 ? 4 : 2);
+      if (!F32) {
+        // bf16: pack the first 64 columns while the second 64 are loaded, release
+        // the accumulator after the last TMEM read, then store (TMEM reads run at
+        // ~64 B/clk, so no store sits between them)
+        uint32_t pk[32], v[64];
+        tmem_ld64(v, tbase);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(v[2 * i]), alpha * __uint_as_float(v[2 * i + 1]));
+          pk[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        tmem_ld64(v, tbase + 64);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(bar_acce);          // MMA may overwrite the accumulator
+        if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
+        if (gm >= g.M) continue;
+        __nv_bfloat16* dr = reinterpret_cast<__nv_bfloat16*>(drow);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {                        // 8 columns per 16-byte store
+          uint32_t p[4];
+          if (c < 8) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = pk[4 * c + i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j = 8 * (c - 8) + 2 * i;
+              __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(v[j]), alpha * __uint_as_float(v[j + 1]));
+              p[i] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          const int n = gn0 + 8 * c;
+          if (n + 8 <= g.N) {
+            *reinterpret_cast<uint4*>(dr + n) = make_uint4(p[0], p[1], p[2], p[3]);
+          } else {
+            for (int i = 0; i < 8 && n + i < g.N; ++i) dr[n + i] = reinterpret_cast<const __nv_bfloat16*>(p)[i];
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int half = 0; half < 2; ++half) {                  // 64 columns per pass
         uint32_t v[2][32];
-        Q2_LD32(v[0], tbase + half * 64);
-        Q2_LD32(v[1], tbase + half * 64 + 32);
+        tmem_ld64(&v[0][0], tbase + half * 64);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (half == 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(bar_acce);        // MMA may overwrite the accumulator
+          if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
         }
         if (gm >= g.M) continue;
 #pragma unroll
@@ -367,8 +437,20 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
       !make_map(&maps[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, b->codes, b->K / 2, b->R, b->K / 2, BKB, 128) ||
       !make_sf_map(&maps[2], a->sf, a->R, a->K, 1, 16) || !make_sf_map(&maps[3], b->sf, b->R, b->K, 2, 16))
     return Q2_ECUDA;
+  static unsigned long long* trace = nullptr;
+  if (getenv("Q2_GEMM_TRACE") && !trace) cudaMalloc(&trace, 64 * 4 * 8);
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
-             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate};
+             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_TRACE") ? trace : nullptr};
+  if (g.trace) cudaMemsetAsync(trace, 0, 64 * 4 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  return d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
+  const int rc = d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
+  if (g.trace) {
+    unsigned long long h[256];
+    cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 12; ++i)
+      fprintf(stderr, "tile %d: mma %.2f us, accf->wake %.2f, wake->release %.2f, release->next start %.2f\n", i,
+              (h[4 * i + 1] - h[4 * i]) / 1e3, (h[4 * i + 2] - h[4 * i + 1]) / 1e3, (h[4 * i + 3] - h[4 * i + 2]) / 1e3,
+              (h[4 * i + 4] - h[4 * i + 3]) / 1e3);
+  }
+  return rc;
 }
