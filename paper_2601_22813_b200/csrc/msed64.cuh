@@ -63,7 +63,8 @@ struct M64Tile {
   static constexpr int OFF_DEC = STAGES * RAW;
   static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 16 x 640 B
   static constexpr int OFF_SGN = OFF_CST + M64_WARPS * 640;              // 4 x 16 sign words
-  static constexpr int OFF_BAR = OFF_SGN + 256;
+  static constexpr int OFF_SPAN = OFF_SGN + 256;                          // tape: 3 x 8 groups x (min, max)
+  static constexpr int OFF_BAR = OFF_SPAN + 3 * 8 * 8;
   static constexpr int SMEM = OFF_BAR + 128 + 1024;
 };
 
@@ -185,6 +186,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
     mbar_fence_init();
   }
+  if (SRC == Q2_SRC_TAPE_COLS && threadIdx.x < 48)
+    reinterpret_cast<int*>(smem + TL::OFF_SPAN)[threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
   if (threadIdx.x < 64) {
     const int qq = threadIdx.x >> 4, k = threadIdx.x & 15, e = 8 * k + 2 * qq;
     const uint32_t s0 = (a.sign[e >> 5] >> (e & 31)) & 1u, s1 = (a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u;
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     const uint32_t st = smem_u32(smem + s * TL::RAW);
     const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
     double y[16][2];
+    bool fwht_done = false;
 
     if (SRC == Q2_SRC_TAPE_COLS) {
       // decode the NVFP4 tape block [128 tape rows x 128 tape cols] into f16 (exact:
@@ -280,10 +284,25 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
                                                                 ((tri >> 5) << 2));
         const uint32_t neg = ((a.sign[tri >> 5] >> (tri & 31)) & 1u) ? 0x80008000u : 0u;
         uint32_t sc[2];
+        // per-group binade range of the tile's scales, triple-buffered: buffer
+        // (it+1)%3 was last read in iteration it-2, which every warp finished
+        // before the previous tile's barrier
+        int* span = reinterpret_cast<int*>(smem + TL::OFF_SPAN) + 16 * (it % 3);
+        if (threadIdx.x < 16)
+          reinterpret_cast<int*>(smem + TL::OFF_SPAN)[16 * ((it + 1) % 3) + threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           const uint32_t s8 = (sfw >> (8 * (2 * (h & 1) + g))) & 0xFF;
           asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(sc[g]) : "h"((unsigned short)(s8 | (s8 << 8))));
+          // binade of the scale (E4M3 subnormals m 2^-9 included); zero scales do not count
+          const int e = (s8 >> 3) ? (int)(s8 >> 3) - 7 : 22 - __clz(s8 & 7u);      // subnormal m 2^-9: floor(log2 m) - 9
+          int emin = s8 ? e : 64, emax = s8 ? e : -64;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+            emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
+          }
+          if (lane == 0) { atomicMin(&span[2 * (2 * h + g)], emin); atomicMax(&span[2 * (2 * h + g) + 1], emax); }
         }
         const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
         uint32_t o[16];
@@ -304,18 +323,61 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       if (lane == 0) mbar_arrive(bar_empty + 8 * s);
       named_bar(1, M64_THREADS);
       const uint32_t db = smem_u32(dec);
+      // Exact fp32 route: FP4*E4M3 values have <= 6 significant bits, so when the
+      // tile's scales for this warp's group span <= 7 binades every partial sum of
+      // the 128-point transform fits 24 bits: the fp32 FWHT of the unscaled values
+      // is exact, and fl64(fl64(sum * scale32) * c) is the reference's
+      // fl64(FWHT(x * scale32) * c) (all of its float64 partial sums are exact too).
+      const int* sp = reinterpret_cast<const int*>(smem + TL::OFF_SPAN) + 16 * (it % 3) + 2 * (warp >> 1);
+      fwht_done = sp[1] - sp[0] <= 7;                          // warp-uniform (one group per warp)
+      float z[16][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t v[4];
         const int k = 4 * i + (lane >> 3), ri = lane & 7;
         ldsm_x4_t(db + (warp >> 3) * 16384 + (8 * k + ri) * 128 + (((warp & 7) ^ ri) << 4), v);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float f0, f1;
+        for (int j = 0; j < 4; ++j)
           asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-              : "=f"(f0), "=f"(f1) : "r"(v[j]));
-          y[4 * i + j][0] = __dmul_rn((double)f0, tape_s);
-          y[4 * i + j][1] = __dmul_rn((double)f1, tape_s);
+              : "=f"(z[4 * i + j][0]), "=f"(z[4 * i + j][1]) : "r"(v[j]));
+      }
+      if (fwht_done) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float u = z[k][0], v = z[k][1];
+          z[k][0] = u + v;
+          z[k][1] = u - v;
+        }
+#pragma unroll
+        for (int m = 1; m <= 2; m <<= 1) {
+          const float sgn = (q & m) ? -1.f : 1.f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) z[k][b] = fmaf(sgn, z[k][b], __shfl_xor_sync(0xFFFFFFFFu, z[k][b], m));
+        }
+#pragma unroll
+        for (int hk = 1; hk < 16; hk <<= 1)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            if (k & hk) continue;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const float u = z[k][b], v = z[k + hk][b];
+              z[k][b] = u + v;
+              z[k + hk][b] = u - v;
+            }
+          }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          y[k][0] = __dmul_rn(__dmul_rn((double)z[k][0], tape_s), c_eff);
+          y[k][1] = __dmul_rn(__dmul_rn((double)z[k][1], tape_s), c_eff);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          y[k][0] = __dmul_rn((double)z[k][0], tape_s);
+          y[k][1] = __dmul_rn((double)z[k][1], tape_s);
         }
       }
     } else if (DT == Q2_BF16) {
@@ -365,6 +427,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
 
     // ---------------------------------------------------------------- FWHT
+    if (!fwht_done) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {                   // h = 1 (bit b)
       const double u = y[k][0], v = y[k][1];
@@ -398,6 +461,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     for (int k = 0; k < 16; ++k) {
       y[k][0] = __dmul_rn(y[k][0], c_eff);
       y[k][1] = __dmul_rn(y[k][1], c_eff);
+    }
     }
 
     // ------------------------------------------------------- group maxima

@@ -100,11 +100,13 @@ def test_ms_eden_cols(cuda, mode, family):
     assert_same(got, ref, f"msed cols {mode}")
 
 
+@pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("mode", ["exact", "posthoc"])
-def test_ms_eden_tape(cuda, mode):
-    """W^T / X^T re-quantized from the saved NVFP4 tape (source='tape')."""
+def test_ms_eden_tape(cuda, mode, family):
+    """W^T / X^T re-quantized from the saved NVFP4 tape (source='tape'); narrow-range
+    families take the exact fp32 transform, wide-range ones the float64 one."""
     q2 = _q2()
-    w = make("lognormal_rows", (256, 192), seed=9)      # tape logical [K=256, R=192]
+    w = make(family, (256, 192), seed=9)                # tape logical [K=256, R=192]
     qw = q2.quantize_rtn_46(_dev(w))
     got = q2.msed(qw, q2.SeedPair(5, 6), 6.0, 30, 40, mode, "tape")
     deq = O.dequantize(O.quantize_rtn_46(w))
