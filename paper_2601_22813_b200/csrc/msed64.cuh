@@ -253,9 +253,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   const float is_lo = __frcp_rd(__double2float_ru(a.s)), is_hi = __frcp_ru(__double2float_rd(a.s));
   const float isd_lo = __frcp_rd(__double2float_ru(sdiv)), isd_hi = __frcp_ru(__double2float_rd(sdiv));
   const int64_t gpr = a.K / GROUP;
-  constexpr bool SCALED = DT == Q2_BF16 && SRC != Q2_SRC_TAPE_COLS;     // inputs carried as x * 2^-896
-  const double c_eff = SCALED ? __dmul_rn(a.inv_sqrt, 0x1p896) : a.inv_sqrt;
-  uint32_t m16 = 0;                                  // bf16 |x| bits max (non-finite check)
+  const double c_eff = a.inv_sqrt;
   uint64_t wabs = 0, wp = 0;                          // running |y| max / pseudo max (f64 bits)
   bool bad = false, ovf = false, nanscale = false;
 
@@ -391,14 +389,9 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           ldsm_x4_t(st + (warp >> 3) * 16384 + (8 * k + ri) * 128 + (((warp & 7) ^ ri) << 4), v);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          // bf16 -> float64 * 2^-896 by moving the fields (exact, zeros and subnormals
-          // included); 2^896 is folded into the final 128**-0.5 multiply
-          const uint32_t w = v[j] ^ sgt[4 * i + j];
-          asm("max.u16x2 %0, %0, %1;" : "+r"(m16) : "r"(w & 0x7FFF7FFFu));
-          const uint32_t h0 = ((w << 16) & 0x80000000u) | ((w << 13) & 0x0FFFE000u);
-          const uint32_t h1 = (w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u);
-          y[4 * i + j][0] = bitsd((uint64_t)h0 << 32);
-          y[4 * i + j][1] = bitsd((uint64_t)h1 << 32);
+          const uint32_t w = v[j] ^ sgt[4 * i + j];          // random signs (exact: sign-bit flips)
+          y[4 * i + j][0] = (double)__uint_as_float(w << 16);
+          y[4 * i + j][1] = (double)__uint_as_float(w & 0xFFFF0000u);
         }
       }
       __syncwarp();
@@ -723,7 +716,6 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     if (MODE != M64_QUANT && wabs) atomicMax(&a.red[0], (unsigned long long)wabs);
     if ((MODE == M64_PMAX || MODE == M64_POSTHOC) && wp) atomicMax(&a.red[1], (unsigned long long)wp);
   }
-  if (SCALED && ((m16 & 0xFFFFu) >= 0x7F80u || (m16 >> 16) >= 0x7F80u)) bad = true;
   if (bad) atomic_or_err(a.err, Q2_ERR_NONFINITE);
   if (ovf) atomic_or_err(a.err, MODE == M64_QUANT ? Q2_ERR_SCALE448 : Q2_ERR_E8M3_OVF);
   if (nanscale) atomic_or_err(a.err, Q2_ERR_NAN_SCALE);
