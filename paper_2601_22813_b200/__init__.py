@@ -7,7 +7,7 @@ meanings, computed by hand-written sm_100a CUDA in ``libquartet2.so``.
 
 from .rht import CHUNK, SeedPair, derive_stream, prng_uniform, sign_mask
 from .quantizers import (GROUP, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
-                         quantize_rtn, quantize_rtn_46, set_error_mode)
+                         deserialize_nvfp4, quantize_rtn, quantize_rtn_46, serialize_nvfp4, set_error_mode)
 from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
                       pass1, pass2,
                       posthoc_quantize)
@@ -19,5 +19,5 @@ __all__ = [
     "sign_mask", "NVFP4Tensor", "quantize_rtn", "quantize_rtn_46", "dequantize", "check_errors",
     "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual_posthoc", "pass1", "pass2", "posthoc_quantize",
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
-    "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW",
+    "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
 ]

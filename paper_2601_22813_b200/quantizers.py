@@ -10,6 +10,7 @@ exactly representable in float32.
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -146,8 +147,8 @@ class NVFP4Tensor:
 
     @classmethod
     def from_reference(cls, fp4, scales8, scale32, device="cuda") -> "NVFP4Tensor":
-        fp4 = torch.as_tensor(np.ascontiguousarray(fp4, dtype=np.uint8)).to(device)
-        s8 = torch.as_tensor(np.ascontiguousarray(scales8, dtype=np.uint8)).to(device)
+        fp4 = torch.from_numpy(np.array(fp4, dtype=np.uint8, order="C")).to(device)
+        s8 = torch.from_numpy(np.array(scales8, dtype=np.uint8, order="C")).to(device)
         t = cls.empty(tuple(fp4.shape), device)
         t.scale.fill_(float(np.float32(scale32)))
         tc = t.c()
@@ -226,3 +227,42 @@ def dequantize(t: NVFP4Tensor) -> torch.Tensor:
     tc = t.c()
     _lib.check(_lib.lib().q2_dequant(ctypes.byref(tc), out.data_ptr(), stream_handle()), "dequant")
     return out.reshape(t.shape)
+
+
+# ---------------------------------------------------------------- container ---
+_MAGIC, _VERSION = b"NV4T", 1
+
+
+def serialize_nvfp4(t: NVFP4Tensor) -> bytes:
+    """The NV4T binary container (quantizers.py:326-349): magic, u16 version,
+    u8 ndim, u8 group axis (0xFF = last), ndim x u32 dims, codes packed two per
+    byte (low nibble first -- the device layout as is), E4M3 scale bytes
+    row-major, fp32 tensor scale, all little-endian."""
+    if not isinstance(t, NVFP4Tensor):
+        raise TypeError(f"cannot serialize {type(t).__name__}")
+    _, s8 = t.unpacked()
+    head = struct.pack(f"<4sHBB{len(t.shape)}I", _MAGIC, _VERSION, len(t.shape), 0xFF, *t.shape)
+    return (head + t.codes.contiguous().cpu().numpy().tobytes() + s8.cpu().numpy().tobytes()
+            + struct.pack("<f", float(t.scale32)))
+
+
+def deserialize_nvfp4(buf: bytes, device="cuda") -> NVFP4Tensor:
+    """Inverse of serialize_nvfp4 (quantizers.py:352-372), onto the device."""
+    magic, version, ndim, _axis = struct.unpack_from("<4sHBB", buf, 0)
+    if magic != _MAGIC:
+        raise ValueError("bad magic in NVFP4 container")
+    if version != _VERSION:
+        raise ValueError(f"unsupported NVFP4 container version {version}")
+    dims = struct.unpack_from(f"<{ndim}I", buf, 8)
+    n = int(np.prod(dims))
+    off = 8 + 4 * ndim
+    packed = np.frombuffer(buf, dtype=np.uint8, count=n // 2, offset=off)
+    codes = np.empty(n, dtype=np.uint8)
+    codes[0::2] = packed & 0xF
+    codes[1::2] = packed >> 4
+    off += n // 2
+    s8 = np.frombuffer(buf, dtype=np.uint8, count=n // GROUP, offset=off)
+    off += n // GROUP
+    (scale32,) = struct.unpack_from("<f", buf, off)
+    return NVFP4Tensor.from_reference(codes.reshape(dims), s8.reshape(*dims[:-1], dims[-1] // GROUP),
+                                      np.float32(scale32), device)

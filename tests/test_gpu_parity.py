@@ -214,3 +214,20 @@ def test_ms_eden_rows_cols_dual(cuda, family):
     qr, qc = q2.msed_dual_posthoc(_dev(e), s, 3, 4, 5, 6)
     assert_same(qr, O.posthoc_quantize(e, rs, 6.0, 3, 4), "dual rows")
     assert_same(qc, O.posthoc_quantize(et, rs, 6.0, 5, 6), "dual cols")
+
+
+@pytest.mark.parametrize("family", ["normal", "zero_rows", "tiny_chunk"])
+def test_nv4t_container(cuda, family):
+    """serialize_nvfp4 / deserialize_nvfp4 (quantizers.py:326-372): byte-identical
+    to the reference container of the same quantization, and a lossless round trip."""
+    q2 = _q2()
+    x = make(family, (192, 256), seed=21)
+    t = q2.quantize_rtn_46(_dev(x))
+    blob = q2.serialize_nvfp4(t)
+    assert blob == O.serialize_nvfp4(O.quantize_rtn_46(x))
+    back = q2.deserialize_nvfp4(blob)
+    for a, b in zip(back.to_reference(), t.to_reference()):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    assert torch.equal(back.codes, t.codes)
+    with pytest.raises(ValueError, match="magic"):
+        q2.deserialize_nvfp4(b"XXXX" + blob[4:])
