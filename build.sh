@@ -16,7 +16,7 @@ for f in $SRC; do
   done
   if [ "$stale" = 1 ]; then
     "$NVCC" -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC \
-      -Xptxas -v -diag-suppress 128 -c "$f" -o "$o" 2> "build/$(basename "${f%.cu}").ptxas.log" || { cat "build/$(basename "${f%.cu}").ptxas.log"; exit 1; }
+      -Xptxas -v -diag-suppress 128 ${Q2_NVCC_FLAGS:-} -c "$f" -o "$o" 2> "build/$(basename "${f%.cu}").ptxas.log" || { cat "build/$(basename "${f%.cu}").ptxas.log"; exit 1; }
   fi
   objs="$objs $o"
 done

@@ -27,6 +27,29 @@ BACKWARD_SCHEMES = ("ms_eden",)
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
 
+# The two independent chains of each pass (Q(X) | Q(W); dX chain | dW chain)
+# run on the caller's stream and one side stream per device, forked and joined
+# with events (captured as parallel branches under CUDA-graph capture), so one
+# chain's small kernels and tails fill the SMs the other leaves idle.
+_SIDE_STREAMS = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    key = torch.device(device).index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _SIDE_STREAMS[key]
+
+
+def _keep(main: torch.cuda.Stream, *tensors) -> None:
+    """Memory made on the side stream is later used on ``main``."""
+    for t in tensors:
+        if isinstance(t, NVFP4Tensor):
+            for u in (t.codes, t.sf, t.scale):
+                u.record_stream(main)
+        elif isinstance(t, torch.Tensor):
+            t.record_stream(main)
+
 
 @dataclass(frozen=True)
 class LayerConfig:
@@ -118,8 +141,14 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     own = err is None
     if own:
         err = _err_word(x2.device)
+    main = torch.cuda.current_stream(x2.device)
+    side = _side_stream(x2.device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        qw = quantize_rtn_46(w2, _err=err)
     qx = quantize_rtn_46(x2, _err=err)
-    qw = quantize_rtn_46(w2, _err=err)
+    main.wait_stream(side)
+    _keep(main, qw)
     y = gemm(qx, qw, out_dtype)
     if own:
         _finish(err)
@@ -139,14 +168,23 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     own = err is None
     if own:
         err = _err_word(e2.device)
+    main = torch.cuda.current_stream(e2.device)
+    side = _side_stream(e2.device)
+    side.wait_stream(main)
+    # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
+    with torch.cuda.stream(side):
+        qet = msed(e2, seeds, 6.0, derive_stream(PAIR_DW, 0), PAIR_DW, mode, "cols", err)
+        qxt = msed(tape.qX, seeds, 6.0, derive_stream(PAIR_DW, 1), PAIR_DW, mode, "tape", err)
+        dw = gemm(qet, qxt, torch.float32)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
     qe = msed(e2, seeds, 6.0, derive_stream(PAIR_DX, 0), PAIR_DX, mode, "rows", err)
     qwt = msed(tape.qW, seeds, 6.0, derive_stream(PAIR_DX, 1), PAIR_DX, mode, "tape", err)
     dx = gemm(qe, qwt, dx_dtype)
-    # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens
-    qet = msed(e2, seeds, 6.0, derive_stream(PAIR_DW, 0), PAIR_DW, mode, "cols", err)
-    qxt = msed(tape.qX, seeds, 6.0, derive_stream(PAIR_DW, 1), PAIR_DW, mode, "tape", err)
-    dw = gemm(qet, qxt, torch.float32)
+    main.wait_stream(side)
+    _keep(main, dw)
+    e2.record_stream(side)
+    for t in (tape.qX,):
+        _keep(side, t)
     if own:
         _finish(err)
     return GradPair(dx, dw)

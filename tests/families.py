@@ -2,7 +2,7 @@
 
 import numpy as np
 
-FAMILIES = ("normal", "lognormal_rows", "coarse_grid", "zero_rows", "outliers", "tiny_chunk", "t2")
+FAMILIES = ("normal", "lognormal_rows", "coarse_grid", "zero_rows", "outliers", "tiny_chunk", "t2", "tie_grid")
 
 
 def make(family: str, shape, seed: int = 0, bf16: bool = True) -> np.ndarray:
@@ -25,6 +25,12 @@ def make(family: str, shape, seed: int = 0, bf16: bool = True) -> np.ndarray:
         x[:, :128] *= 1e-7
     elif family == "t2":
         x = rng.standard_t(2.0, (r, k))
+    elif family == "tie_grid":
+        # absmax 5.25 = 21 * 2^-2 makes scale32 a few-bit number (17 * 2^-13 for
+        # the 4/6 quantizer), so values on a 2^-6 grid land exactly on E2M1
+        # rounding thresholds and E4M3 midpoints
+        x = np.clip(np.round(x * 64.0) / 64.0, -5.25, 5.25)
+        x.flat[0] = 5.25
     elif family != "normal":
         raise ValueError(family)
     x = x.astype(np.float32)
