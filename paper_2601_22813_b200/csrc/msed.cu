@@ -130,6 +130,7 @@ static M64Args base_args(const M64Src& s, int64_t R, int64_t K, const uint32_t s
   if (s.kind == Q2_SRC_TAPE_COLS) { a.tape_sf = s.tape->sf; a.tape_scale32 = s.tape->scale32; }
   a.tiles_r = (int)((R + M64_ROWS - 1) / M64_ROWS);
   a.tiles_c = (int)(K / CHUNK);
+  a.fc = FastDiv((uint32_t)a.tiles_c);
   return a;
 }
 

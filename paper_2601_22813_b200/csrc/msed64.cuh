@@ -53,6 +53,7 @@ struct M64Args {
   unsigned long long* red;                        // [0] |x_rot| max, [1] pseudo max (f64 bits)
   uint32_t* err;
   int tiles_r, tiles_c;
+  FastDiv fc;                                     // division by tiles_c
 };
 
 template <int SRC, int DT>
@@ -200,12 +201,12 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   // Thread 0 refills the ring: tile i goes to stage i % STAGES once all warps
   // released that stage's previous tile (they do so right after reading it).
   const int64_t sf_kb = sf_kblocks(a.R);
+  // tile i of this CTA goes to stage i % STAGES once every warp released that
+  // stage's previous tile (they arrive right after reading it)
   auto issue = [&](int i) {
     const int t = blockIdx.x + i * gridDim.x;
-    if (t >= ntiles) return;
-    const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
+    const int tr = (int)a.fc.div((uint32_t)t), tc = t - tr * a.tiles_c;
     const int s = i % TL::STAGES;
-    if (i >= TL::STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((i / TL::STAGES) - 1) & 1);
     const uint32_t dst = smem_u32(smem + s * TL::RAW), fb = bar_full + 8 * s;
     // tape: the second 1 KiB scale block does not exist when R % 128 == 64
     const int sfb = SRC == Q2_SRC_TAPE_COLS ? (2 * tr + 1 < sf_kb ? 2048 : 1024) : 0;
@@ -221,9 +222,25 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       bulk_load(dst + 8192, a.tape_sf + ((((int64_t)tc >> 1) * sf_kb + 2 * tr) << 10), sfb, fb);
     }
   };
+  // Thread 0 (also a consumer) keeps the ring full without blocking on a slow
+  // warp: refills whose stage is still in use are retried at the next pump,
+  // except the one the current tile needs.
+  const int nmine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  int next = 0;
+  auto pump = [&](int it, bool must) {
+    while (next < nmine && next < it + TL::STAGES) {
+      const int s = next % TL::STAGES;
+      if (next >= TL::STAGES) {
+        const uint32_t par = ((next / TL::STAGES) - 1) & 1;
+        if (must && next <= it) mbar_wait_sleep(bar_empty + 8 * s, par);
+        else if (!mbar_test(bar_empty + 8 * s, par)) break;
+      }
+      issue(next++);
+    }
+  };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
-    for (int i = 0; i < TL::STAGES - 1; ++i) issue(i);
+    pump(0, true);
   }
 
   // -------------------------------------------------------------- consumers
@@ -259,9 +276,9 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
 
   int it = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int tr = t / a.tiles_c, tc = t - tr * a.tiles_c;
+    const int tr = (int)a.fc.div((uint32_t)t), tc = t - tr * a.tiles_c;
     const int s = it % TL::STAGES;
-    if (threadIdx.x == 0) issue(it + TL::STAGES - 1);
+    if (threadIdx.x == 0) pump(it, true);
     mbar_wait_sleep(bar_full + 8 * s, (it / TL::STAGES) & 1);
     const uint32_t st = smem_u32(smem + s * TL::RAW);
     const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
@@ -456,6 +473,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       y[k][1] = __dmul_rn(y[k][1], c_eff);
     }
     }
+
+    if (threadIdx.x == 0) pump(it, false);
 
     // ------------------------------------------------------- group maxima
     // From the float64 high words: gmax lies in [H 2^32, (H+1) 2^32) for the
