@@ -42,6 +42,14 @@ def main():
             pack(key + "pow2_", ME.ms_eden_quantize(x, seeds, tensor_id=77, rotation_id=99, pow2_scale=True), out)
             er, red = PH.pass1(x, seeds.rht, tensor_id=77, rotation_id=99)
             pack(key + "posthoc_", PH.pass2(er, red, seeds.sr, tensor_id=77), out)
+            # stochastic-rounding baselines (quantizers.py:139-161, :237-262); the
+            # non-clipping AssertionError is recorded as a flag
+            for tag, fn in (("sr_", lambda v: R.quantize_sr(v, 123, 7)), ("sr46_", lambda v: R.quantize_sr_46(v, 123, 7)),
+                            ("srrht_", lambda v: R.quantize_sr(RH.rht_apply(v, 11, 3), 5, 9))):
+                try:
+                    pack(key + tag, fn(x), out)
+                except AssertionError:
+                    out[key + tag + "assert"] = np.ones(1, dtype=np.uint8)
     # end-to-end digest case of SURVEY.md §8(c)
     rng = np.random.default_rng(2026)
     X = rng.standard_normal((128, 256)).astype(np.float32)
@@ -52,6 +60,10 @@ def main():
     out.update(e2e_X=X, e2e_W=W, e2e_E=E, e2e_Y=y, e2e_dX=g.dX, e2e_dW=g.dW)
     pack("e2e_qX_", tape.qX, out)
     pack("e2e_qW_", tape.qW, out)
+    # tetrajet_v2 baseline (rtn_1x16 forward, sr_rht backward) on the same data
+    y, tape = LG.forward(X, W, LG.baseline_config("tetrajet_v2"))
+    g = LG.backward(tape, E, RH.SeedPair(7, 9))
+    out.update(tj_Y=y, tj_dX=g.dX, tj_dW=g.dW)
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))
