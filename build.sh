@@ -4,7 +4,7 @@ set -euo pipefail
 cd "$(dirname "$0")"
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 OUT=paper_2601_22813_b200/libquartet2.so
-SRC="paper_2601_22813_b200/csrc/quant_fwd.cu paper_2601_22813_b200/csrc/msed.cu paper_2601_22813_b200/csrc/gemm.cu paper_2601_22813_b200/csrc/helpers.cu"
+SRC="paper_2601_22813_b200/csrc/quant_fwd.cu paper_2601_22813_b200/csrc/msed.cu paper_2601_22813_b200/csrc/gemm.cu paper_2601_22813_b200/csrc/helpers.cu paper_2601_22813_b200/csrc/sr.cu"
 mkdir -p build
 objs=""
 for f in $SRC; do

@@ -52,7 +52,8 @@ enum {
   Q2_ERR_NONFINITE = 1u,  /* "input must be finite"              quantizers.py:118-119 */
   Q2_ERR_SCALE448  = 2u,  /* corrected scale exceeds 448         ms_eden.py:144-149, posthoc.py:115-122 */
   Q2_ERR_NAN_SCALE = 4u,  /* NaN reached encode_fp8_rtn          formats.py:167-168 */
-  Q2_ERR_E8M3_OVF  = 8u   /* round_e8m3_rtn overflow             formats.py:223-224 */
+  Q2_ERR_E8M3_OVF  = 8u,  /* round_e8m3_rtn overflow             formats.py:223-224 */
+  Q2_ERR_SR_CLIP   = 16u  /* SR group quotient above 6 (AssertionError "encoder bug") quantizers.py:153-157 */
 };
 
 typedef struct {
@@ -133,13 +134,39 @@ int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr, const uint
  *  out_rows = pass2(pass1(E))      rows of E along N  (dgrad operand, pair_dx)
  *  out_cols = pass2(pass1(E^T))    rows of E^T along T (wgrad operand, pair_dw)
  * (linear_graph.py:306 and :325 with the posthoc.py:74-125 quantizer).  E is
- * bf16 [T, N] (row stride ld), T % 128 == N % 128 == 0.  The Hadamard rotations
- * run on the tensor cores (tcgen05 kind::f16 against resident H.diag(signs)).
+ * bf16 [T, N] (row stride ld), T % 128 == N % 128 == 0; two q2_msed_quant
+ * passes (rows and columns source) with their own sign vectors and streams.
  * ws_rows / ws_cols: q2_msed_ws_bytes(T, N) / q2_msed_ws_bytes(N, T).          */
 int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
                          const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
                          uint64_t sr_stream_rows, uint64_t sr_stream_cols, const q2_nvfp4* out_rows,
                          const q2_nvfp4* out_cols, void* ws_rows, void* ws_cols, uint32_t* err, void* stream);
+
+/* Stochastic-rounding baselines.
+ *   q2_quant_sr: quantize_sr (quantizers.py:139-161; ncaps 1, cap0 6) and
+ *   quantize_sr_46 (:237-262; ncaps 2, caps 6/4) on bf16/fp32 rows [R, K]
+ *   (ld == K, 32-byte aligned):
+ *     scale32 = (float)(absmax / scale_div)
+ *     s8_b    = E4M3_RTN(gmax / ((scale32 * cap_b) * margin))   float64
+ *     codes   = _nb_sr (_kernels.py:130-157) with
+ *               u = prng_uniform(seed, stream_b, flat index)  (rht.py:89-96)
+ *     46: per group the branch with strictly lower float64 error (ties: 0).
+ *   The caller passes scale_div and margin evaluated in the reference's
+ *   float64 order (6 * (16/17) * 448 for quantize_sr, 6 * (448 * 16/17) for
+ *   quantize_sr_46; margin 16/17).  A group quotient above 6 (ncaps 1) sets
+ *   Q2_ERR_SR_CLIP.  ws: q2_quant_sr_ws_bytes() bytes.
+ *   q2_rht_sr_quant: the sr_rht operand quantizer (linear_graph.py:259-274):
+ *   x_rot = rht_apply(x, sign_mask) along K (rht.py:144-155), then quantize_sr
+ *   of x_rot with the same constants; sources as q2_msed_quant.  Two passes
+ *   over x (absmax of x_rot, then quantize).  ws: q2_msed_ws_bytes(R, K).    */
+size_t q2_quant_sr_ws_bytes(void);
+int q2_quant_sr(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0, double cap1,
+                double margin, double scale_div, uint64_t seed, uint64_t stream0, uint64_t stream1,
+                const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);
+int q2_rht_sr_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K,
+                    int64_t ld, const uint32_t sign_mask[4], double cap, double margin, double scale_div,
+                    double inv_sqrt_chunk, uint64_t seed, uint64_t stream, const q2_nvfp4* out, void* ws,
+                    uint32_t* err, void* stream_);
 
 /* NVFP4 "TN" GEMM on tcgen05 block-scaled MMAs (kind::mxf4nvf4, UE4M3 scales
  * per 16, FP32 accumulation in TMEM):  D[M, N] = alpha * A[M,K] . B[N,K]^T

@@ -17,13 +17,14 @@ Q2_OK, Q2_EINVAL, Q2_ECUDA = 0, 1, 2
 Q2_BF16, Q2_F32 = 0, 1
 Q2_SRC_ROWS, Q2_SRC_COLS, Q2_SRC_TAPE_COLS = 0, 1, 2
 Q2_MSED_EXACT, Q2_MSED_POW2, Q2_MSED_POSTHOC = 0, 1, 2
-Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF = 1, 2, 4, 8
+Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF, Q2_ERR_SR_CLIP = 1, 2, 4, 8, 16
 
 # Every symbol include/quartet2.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "q2_sf_bytes", "q2_version", "q2_amax", "q2_quant_fwd_ws_bytes", "q2_quant_fwd",
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
     "q2_msed_dual_posthoc", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
+    "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant",
 )
 
 
@@ -55,6 +56,10 @@ _SIGS = {
     "q2_msed_dual_posthoc": (_I, [_P, _I64, _I64, _I64, _U32x4, _U32x4, _D, _D, _U64, _U64, _U64, _TP, _TP, _P, _P,
                                   _P, _P]),
     "q2_gemm_tn": (_I, [_TP, _TP, _P, _I, _I64, _I, _P]),
+    "q2_quant_sr_ws_bytes": (ctypes.c_size_t, []),
+    "q2_quant_sr": (_I, [_P, _I, _I64, _I64, _I64, _I, _D, _D, _D, _D, _U64, _U64, _U64, _TP, _P, _P, _P]),
+    "q2_rht_sr_quant": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _D, _D, _U64, _U64, _TP, _P, _P,
+                             _P]),
     "q2_dequant": (_I, [_TP, _P, _P]),
     "q2_unpack": (_I, [_TP, _P, _P, _P]),
     "q2_pack": (_I, [_P, _P, _TP, _P]),

@@ -118,6 +118,24 @@ __device__ __forceinline__ uint32_t rtn_mag_thresholds(double a, const double* T
   return c;
 }
 
+// Stochastic E2M1 code of v/d with draw u = u53 * 2^-53 (_nb_sr, _kernels.py:130-157):
+// q = fl64(v/d) (q = +0 when d <= 0), a2 = min(2|q|, 12), lo the doubled-grid
+// point at or below a2, step 1/2/4; up iff u < (a2 - lo)/step (exact: a2 - lo is
+// exact by Sterbenz and step a power of two).  *deq = the dequantized value.
+__device__ __forceinline__ uint32_t sr_elem(double v, double d, uint64_t u53, double* deq) {
+  const double q = d > 0.0 ? __ddiv_rn(v, d) : 0.0;
+  const double a2 = fmin(fabs(q) * 2.0, 12.0);
+  const double lo = a2 < 4.0 ? floor(a2) : (a2 < 8.0 ? 2.0 * floor(a2 * 0.5) : 4.0 * floor(a2 * 0.25));
+  const double step = lo < 4.0 ? 1.0 : (lo < 8.0 ? 2.0 : 4.0);
+  const double r = (double)u53 < ((a2 - lo) / step) * 0x1p53 ? lo + step : lo;
+  const uint32_t ri = (uint32_t)r;
+  const uint32_t mag = ri <= 4u ? ri : (ri == 6u ? 5u : (ri == 8u ? 6u : 7u));
+  const bool neg = signbit(q);
+  const double dq = neg ? -r * 0.5 : r * 0.5;
+  *deq = d > 0.0 ? __dmul_rn(dq, d) : 0.0;
+  return mag | (neg ? 8u : 0u);
+}
+
 // ------------------------------------------------------------------- PRNG ---
 // splitmix64 finalizer chain (rht.py:36-39, 57-68, 89-96).
 constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;

@@ -184,6 +184,28 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   return dispatch_m64<M64_QUANT>(src, a, st);
 }
 
+extern "C" int q2_rht_sr_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K,
+                               int64_t ld, const uint32_t sign_mask[4], double cap, double margin, double scale_div,
+                               double inv_sqrt_chunk, uint64_t seed, uint64_t sr_stream, const q2_nvfp4* out,
+                               void* ws, uint32_t* err, void* stream) {
+  if (!out || !ws || !sign_mask || out->R != R || out->K != K) return Q2_EINVAL;
+  const M64Src src{x, dtype, ld, tape, src_kind};
+  int rc = check_src(src, R, K);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  M64Args a = base_args(src, R, K, sign_mask, cap, inv_sqrt_chunk);
+  a.red = reinterpret_cast<unsigned long long*>(w);
+  a.err = err;
+  a.codes = out->codes; a.sf = out->sf; a.scale32 = out->scale32;
+  a.sr_head = prng_head(seed, sr_stream);
+  a.sr_div = scale_div; a.sr_margin = margin;
+  if (cudaMemsetAsync(w, 0, 16, st) != cudaSuccess) return Q2_ECUDA;
+  if (R == 0 || K == 0) return cudaMemsetAsync(out->scale32, 0, 4, st) == cudaSuccess ? Q2_OK : Q2_ECUDA;
+  if ((rc = dispatch_m64<M64_ABSMAX>(src, a, st))) return rc;
+  return dispatch_m64<M64_SR>(src, a, st);
+}
+
 extern "C" int q2_posthoc_pass1(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R,
                                 int64_t K, int64_t ld, const uint32_t sign_mask[4], double s,
                                 double inv_sqrt_chunk, uint8_t* codes, uint16_t* pseudo_bf16, double* corr,

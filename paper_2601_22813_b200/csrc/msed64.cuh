@@ -35,7 +35,7 @@
 
 namespace q2 {
 
-enum { M64_ABSMAX = 0, M64_PMAX = 1, M64_QUANT = 2, M64_POSTHOC = 3 };
+enum { M64_ABSMAX = 0, M64_PMAX = 1, M64_QUANT = 2, M64_POSTHOC = 3, M64_SR = 4 };
 constexpr int M64_ROWS = 128;                     // logical rows per tile (16 warps x 8)
 constexpr int M64_WARPS = 16;
 constexpr int M64_THREADS = 32 * M64_WARPS;
@@ -54,6 +54,7 @@ struct M64Args {
   uint32_t* err;
   int tiles_r, tiles_c;
   FastDiv fc;                                     // division by tiles_c
+  double sr_div, sr_margin;                       // M64_SR: scale32 = amax / sr_div, D = (scale32 * s) * sr_margin
 };
 
 template <int SRC, int DT>
@@ -251,6 +252,14 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   float scale32 = 0.f;
   bool zero = false;                                 // all-zero tensor (quantizers.py:175-176)
   double sdiv = a.s;                                 // gmax / sdiv -> scale candidate
+  double sr_d = 0.0;                                 // M64_SR: the group-scale divisor (scale32 * cap) * margin
+  if (MODE == M64_SR) {
+    const double amax = bitsd(a.red[0]);
+    zero = amax == 0.0;
+    scale32 = zero ? 0.f : __double2float_rn(__ddiv_rn(amax, a.sr_div));
+    sr_d = __dmul_rn(__dmul_rn((double)scale32, a.s), a.sr_margin);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.scale32 = scale32;
+  }
   if (MODE == M64_QUANT) {
     const double amax = bitsd(a.red[0]);
     zero = amax == 0.0;
@@ -490,6 +499,58 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
         m = umax64(m, umax64(dbits(y[k][0]) & 0x7FFFFFFFFFFFFFFFull, dbits(y[k][1]) & 0x7FFFFFFFFFFFFFFFull));
       if (live) wabs = umax64(wabs, m);
       if (MODE == M64_ABSMAX) continue;
+    }
+    if (MODE == M64_SR) {
+      // quantize_sr of x_rot (quantizers.py:139-161): exact float64 group maxima,
+      // literal float64 scale and element divisions, per-element draws.
+      uint64_t gm[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const uint64_t M = 0x7FFFFFFFFFFFFFFFull;
+        uint64_t m = umax64(umax64(dbits(y[2 * g][0]) & M, dbits(y[2 * g][1]) & M),
+                            umax64(dbits(y[2 * g + 1][0]) & M, dbits(y[2 * g + 1][1]) & M));
+        m = umax64(m, __shfl_xor_sync(0xFFFFFFFFu, m, 1));
+        gm[g] = umax64(m, __shfl_xor_sync(0xFFFFFFFFu, m, 2));
+      }
+      uint32_t cw[4] = {0u, 0u, 0u, 0u}, sbw = 0;
+      const uint64_t ibase = (uint64_t)r * (uint64_t)a.K + (uint64_t)tc * CHUNK + 2 * q;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (gm[g] >= 0x7FF0000000000000ull) { if (live) bad = true; continue; }
+        const double gmax = bitsd(gm[g]);
+        const uint32_t sb = zero ? 0u : e4m3_rtn(__ddiv_rn(gmax, sr_d));
+        const double dg = __dmul_rn(e4m3_val(sb), (double)scale32);
+        if (live && dg > 0.0 && __ddiv_rn(gmax, dg) > 6.0 * (1.0 + 1e-9)) ovf = true;   // non-clipping check
+        if (g == 2 * q) sbw |= sb;
+        if (g == 2 * q + 1) sbw |= sb << 8;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = 2 * g + kk;
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const uint64_t u53 = mix64(a.sr_head ^ (ibase + 8 * k + b + GOLDEN)) >> 11;
+            double dq;
+            const uint32_t c = zero ? 0u : sr_elem(y[k][b], dg, u53, &dq);
+            cw[k >> 2] |= c << (8 * (k & 3) + 4 * b);
+          }
+        }
+      }
+      const uint32_t cst = smem_u32(smem + TL::OFF_CST + warp * 640) + rw * 80;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(cst + 4 * k + q), "r"(cw[k >> 2] >> (8 * (k & 3))) : "memory");
+      __syncwarp();
+      uint4 cw4;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(cw4.x), "=r"(cw4.y), "=r"(cw4.z), "=r"(cw4.w)
+                   : "r"(cst + 16 * q) : "memory");
+      __syncwarp();
+      const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, sbw, 1);
+      if (live) {
+        *reinterpret_cast<uint4*>(a.codes + r * (a.K / 2) + (int64_t)tc * 64 + 16 * q) = cw4;
+        if ((q & 1) == 0)
+          *reinterpret_cast<uint32_t*>(a.sf + sf_offset(r, (int64_t)tc * 8 + 2 * q, sf_kblocks(a.K))) = sbw | (other << 16);
+      }
+      continue;
     }
     uint32_t gv[8];
 #pragma unroll
@@ -736,7 +797,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     if ((MODE == M64_PMAX || MODE == M64_POSTHOC) && wp) atomicMax(&a.red[1], (unsigned long long)wp);
   }
   if (bad) atomic_or_err(a.err, Q2_ERR_NONFINITE);
-  if (ovf) atomic_or_err(a.err, MODE == M64_QUANT ? Q2_ERR_SCALE448 : Q2_ERR_E8M3_OVF);
+  if (ovf) atomic_or_err(a.err, MODE == M64_QUANT ? Q2_ERR_SCALE448 : (MODE == M64_SR ? Q2_ERR_SR_CLIP : Q2_ERR_E8M3_OVF));
   if (nanscale) atomic_or_err(a.err, Q2_ERR_NAN_SCALE);
 }
 

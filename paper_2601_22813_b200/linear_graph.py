@@ -21,9 +21,10 @@ from . import _lib
 from .ms_eden import msed
 from .quantizers import NVFP4Tensor, _err_word, _finish, as_device_matrix, quantize_rtn_46, stream_handle
 from .rht import CHUNK, SeedPair, derive_stream
+from .sr import rht_sr
 
-FORWARD_SCHEMES = ("rtn_1x16_46",)
-BACKWARD_SCHEMES = ("ms_eden",)
+FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16")
+BACKWARD_SCHEMES = ("ms_eden", "sr_rht")
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
 
@@ -53,7 +54,8 @@ def _keep(main: torch.cuda.Stream, *tensors) -> None:
 
 @dataclass(frozen=True)
 class LayerConfig:
-    """linear_graph.py:73-99, restricted to the Quartet II recipe this build accelerates."""
+    """linear_graph.py:73-99, restricted to the recipes this build accelerates: quartet2
+    (rtn_1x16_46 + ms_eden) and tetrajet_v2 (rtn_1x16 + sr_rht)."""
 
     forward_scheme: str = "rtn_1x16_46"
     backward_scheme: str = "ms_eden"
@@ -69,14 +71,16 @@ class LayerConfig:
         if self.ablation != "full":
             raise ValueError(f"unknown ablation {self.ablation!r}")
         if self.reuse_forward_weights:
-            raise ValueError("ms_eden requires weight re-quantization")
+            raise ValueError("reuse_forward_weights needs the square-block forward (not built)")
 
 
 def baseline_config(name: str) -> LayerConfig:
-    """linear_graph.py:143-150 (the accelerated recipe: quartet2)."""
+    """linear_graph.py:119-150 for the accelerated recipes."""
     if name == "quartet2":
         return LayerConfig()
-    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2']")
+    if name == "tetrajet_v2":
+        return LayerConfig("rtn_1x16", "sr_rht")
+    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2']")
 
 
 @dataclass
@@ -120,16 +124,23 @@ def gemm_emulated(qa, qb, accumulate: str = "f32") -> torch.Tensor:
     return gemm(qa, qb, torch.float32)
 
 
-def _check_dims(x_shape, w_shape) -> None:
-    """linear_graph.py:224-240 for quartet2 (ms_eden: all rotated dims % 128)."""
+def _check_dims(x_shape, w_shape, cfg: LayerConfig) -> None:
+    """linear_graph.py:224-240: the rotated inner dimensions (out, tokens) are
+    multiples of 128; in must be too for ms_eden (a multiple of 16 otherwise,
+    and of 64 for this build's transposed-tape source)."""
     tokens, in_dim = x_shape
     out_dim, w_in = w_shape
     if w_in != in_dim:
         raise ValueError(f"X is {x_shape} but W is {w_shape}")
-    if in_dim % CHUNK or out_dim % CHUNK or tokens % CHUNK:
+    if in_dim % 16:
+        raise ValueError("in dimension must be a multiple of 16")
+    in_div = CHUNK if cfg.backward_scheme == "ms_eden" else 16
+    if in_dim % in_div or out_dim % CHUNK or tokens % CHUNK:
         raise ValueError(
             f"dims (tokens={tokens}, in={in_dim}, out={out_dim}) are not compatible with backward scheme "
-            f"ms_eden; the rotated inner dimensions must be multiples of {CHUNK}")
+            f"{cfg.backward_scheme}; the rotated inner dimensions must be multiples of {CHUNK}")
+    if in_dim % 64:
+        raise ValueError(f"in dimension {in_dim}: the B200 transposed-tape quantizer needs a multiple of 64")
 
 
 def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out_dtype=torch.float32,
@@ -137,7 +148,8 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     """Quantized forward pass; returns (Y, tape) (linear_graph.py:243-256)."""
     x2, xs, _ = as_device_matrix(x, "X")
     w2, ws, _ = as_device_matrix(w, "W")
-    _check_dims(xs, ws)
+    _check_dims(xs, ws, cfg)
+    caps = (6.0, 4.0) if cfg.forward_scheme.endswith("_46") else (6.0,)   # linear_graph.py:208-221
     own = err is None
     if own:
         err = _err_word(x2.device)
@@ -145,8 +157,8 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     side = _side_stream(x2.device)
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        qw = quantize_rtn_46(w2, _err=err)
-    qx = quantize_rtn_46(x2, _err=err)
+        qw = quantize_rtn_46(w2, caps, _err=err)
+    qx = quantize_rtn_46(x2, caps, _err=err)
     main.wait_stream(side)
     _keep(main, qw)
     y = gemm(qx, qw, out_dtype)
@@ -172,13 +184,19 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     side = _side_stream(e2.device)
     side.wait_stream(main)
     # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
+    if cfg.backward_scheme == "sr_rht":                 # linear_graph.py:259-274 via :310-326
+        def quant(x, pair, operand, source):
+            return rht_sr(x, seeds, derive_stream(pair, operand), pair, source, err)
+    else:                                               # ms_eden, linear_graph.py:304-307, :322-326
+        def quant(x, pair, operand, source):
+            return msed(x, seeds, 6.0, derive_stream(pair, operand), pair, mode, source, err)
     with torch.cuda.stream(side):
-        qet = msed(e2, seeds, 6.0, derive_stream(PAIR_DW, 0), PAIR_DW, mode, "cols", err)
-        qxt = msed(tape.qX, seeds, 6.0, derive_stream(PAIR_DW, 1), PAIR_DW, mode, "tape", err)
+        qet = quant(e2, PAIR_DW, 0, "cols")
+        qxt = quant(tape.qX, PAIR_DW, 1, "tape")
         dw = gemm(qet, qxt, torch.float32)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
-    qe = msed(e2, seeds, 6.0, derive_stream(PAIR_DX, 0), PAIR_DX, mode, "rows", err)
-    qwt = msed(tape.qW, seeds, 6.0, derive_stream(PAIR_DX, 1), PAIR_DX, mode, "tape", err)
+    qe = quant(e2, PAIR_DX, 0, "rows")
+    qwt = quant(tape.qW, PAIR_DX, 1, "tape")
     dx = gemm(qe, qwt, dx_dtype)
     main.wait_stream(side)
     _keep(main, dw)

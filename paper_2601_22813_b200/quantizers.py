@@ -30,6 +30,7 @@ _ERR_MESSAGES = (
     (_lib.Q2_ERR_SCALE448, ValueError,
      "corrected group scale exceeds 448; the 448/256 headroom should absorb the correction factor"),
     (_lib.Q2_ERR_E8M3_OVF, OverflowError, "round_e8m3_rtn overflow beyond the bf16 carrier range"),
+    (_lib.Q2_ERR_SR_CLIP, AssertionError, "non-clipping construction produced quotient above 6; encoder bug"),
 )
 
 # "sync": every public call reads its error word and raises like the reference.

@@ -1,0 +1,89 @@
+"""GPU parity of the stochastic-rounding baselines against the oracle.
+
+quantize_sr / quantize_sr_46 (quantizers.py:139-161, :237-262), the rotated
+sr_rht operand quantizer from every source (linear_graph.py:259-274), and the
+tetrajet_v2 linear pass (rtn_1x16 forward, sr_rht backward).  Codes, scales
+and scale32 bit-exact; GEMM outputs within the tolerance of test_gpu_parity.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import nvfp4_oracle as O
+from tests.families import FAMILIES, make, to_bf16
+from tests.test_gpu_parity import _dev, _q2, assert_same
+
+pytestmark = pytest.mark.gpu
+
+
+def _raises_or_same(gpu_fn, ref_fn, what):
+    try:
+        ref = ref_fn()
+    except AssertionError:
+        with pytest.raises(AssertionError, match="encoder bug"):
+            gpu_fn()
+        return
+    assert_same(gpu_fn(), ref, what)
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("bf16", [True, False])
+def test_quantize_sr(cuda, family, bf16):
+    q2 = _q2()
+    x = make(family, (192, 512), seed=13, bf16=bf16)
+    _raises_or_same(lambda: q2.quantize_sr(_dev(x, bf16), 123, 7), lambda: O.quantize_sr(x, 123, 7), f"sr[{family}]")
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("bf16", [True, False])
+def test_quantize_sr_46(cuda, family, bf16):
+    q2 = _q2()
+    x = make(family, (192, 512), seed=14, bf16=bf16)
+    assert_same(q2.quantize_sr_46(_dev(x, bf16), 321, 5), O.quantize_sr_46(x, 321, 5), f"sr46[{family}]")
+
+
+def test_quantize_sr_zero(cuda):
+    q2 = _q2()
+    z = np.zeros((64, 256), np.float32)
+    assert_same(q2.quantize_sr(_dev(z), 1, 2), O.quantize_sr(z, 1, 2), "sr zero")
+    assert_same(q2.quantize_sr_46(_dev(z), 1, 2), O.quantize_sr_46(z, 1, 2), "sr46 zero")
+
+
+@pytest.mark.parametrize("family", ["normal", "t2", "zero_rows", "outliers", "tie_grid"])
+@pytest.mark.parametrize("source", ["rows", "cols", "tape"])
+def test_rht_sr(cuda, family, source):
+    """quantize_sr(rht_apply(x)) without materialising the rotation or the transpose."""
+    q2 = _q2()
+    seeds = q2.SeedPair(11, 17)
+    x = make(family, (256, 384), seed=15)                       # rows: [R=256, K=384]
+    if source == "rows":
+        gpu_fn = lambda: q2.rht_sr(_dev(x), seeds, 99, 7, "rows")        # noqa: E731
+        logical = x
+    elif source == "cols":
+        gpu_fn = lambda: q2.rht_sr(_dev(x), seeds, 99, 7, "cols")        # noqa: E731  logical x^T [384, 256]
+        logical = np.ascontiguousarray(x.T)
+    else:
+        qx = q2.quantize_rtn_46(_dev(x), caps=(6.0,))
+        gpu_fn = lambda: q2.rht_sr(qx, seeds, 99, 7, "tape")             # noqa: E731  logical dequant(x)^T
+        logical = np.ascontiguousarray(O.dequantize(O.quantize_rtn_46(x, caps=(6.0,))).T)
+    ref_fn = lambda: O.quantize_sr(O.rht_apply(logical, 11, 7), 17, 99)   # noqa: E731
+    _raises_or_same(gpu_fn, ref_fn, f"rht_sr {source} [{family}]")
+
+
+def test_tetrajet_v2_linear(cuda):
+    """rtn_1x16 forward + sr_rht backward (linear_graph.py:119-140 'tetrajet_v2')."""
+    q2 = _q2()
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.baseline_config("tetrajet_v2")
+    y, tape = q2.forward(_dev(x), _dev(w), cfg)
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9))
+    ry, rtape = O.forward(x, w, forward_scheme="rtn_1x16")
+    assert_same(tape.qX, rtape[0], "qX")
+    assert_same(tape.qW, rtape[1], "qW")
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), backward_scheme="sr_rht")
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        got = got.double().cpu().numpy()
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 1e-5, rel
