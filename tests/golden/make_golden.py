@@ -44,6 +44,8 @@ def main():
             pack(key + "posthoc_", PH.pass2(er, red, seeds.sr, tensor_id=77), out)
             # stochastic-rounding baselines (quantizers.py:139-161, :237-262); the
             # non-clipping AssertionError is recorded as a flag
+            for tag, u46 in (("sq_", False), ("sq46_", True)):
+                pack(key + tag, R.quantize_square_block(x, use_46=u46), out)
             for tag, fn in (("sr_", lambda v: R.quantize_sr(v, 123, 7)), ("sr46_", lambda v: R.quantize_sr_46(v, 123, 7)),
                             ("srrht_", lambda v: R.quantize_sr(RH.rht_apply(v, 11, 3), 5, 9))):
                 try:
@@ -64,6 +66,10 @@ def main():
     y, tape = LG.forward(X, W, LG.baseline_config("tetrajet_v2"))
     g = LG.backward(tape, E, RH.SeedPair(7, 9))
     out.update(tj_Y=y, tj_dX=g.dX, tj_dW=g.dW)
+    for name, tag in (("nvidia", "nv"), ("four_over_six", "fos")):
+        y, tape = LG.forward(X, W, LG.baseline_config(name))
+        g = LG.backward(tape, E, RH.SeedPair(7, 9))
+        out.update({f"{tag}_Y": y, f"{tag}_dX": g.dX, f"{tag}_dW": g.dW})
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))
