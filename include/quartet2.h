@@ -168,6 +168,17 @@ int q2_rht_sr_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind
                     double inv_sqrt_chunk, uint64_t seed, uint64_t stream, const q2_nvfp4* out, void* ws,
                     uint32_t* err, void* stream_);
 
+/* 16x16 square-block quantizer (quantize_square_block, quantizers.py:265-312):
+ * one E4M3 scale per 16x16 block, scale32 = (float)(absmax / (6 * 256)), codes
+ * by the literal float64 quotient; use46 picks 6 or 4 per block on the float64
+ * squared error summed in numpy's sum(axis=(1, 3)) order.  Writes the result
+ * twice for the GEMM -- `out` [R, C] and `out_t` = its transpose [C, R], both
+ * with the block scale expanded into the per-16 scale layout -- and the
+ * compact block scales `scales8` uint8 [R/16, C/16].  x bf16/fp32 [R, C]
+ * contiguous, 32-byte aligned.  ws: 16 bytes.                                 */
+int q2_quant_square_block(const void* x, int dtype, int64_t R, int64_t C, int use46, const q2_nvfp4* out,
+                          const q2_nvfp4* out_t, uint8_t* scales8, void* ws, uint32_t* err, void* stream);
+
 /* NVFP4 "TN" GEMM on tcgen05 block-scaled MMAs (kind::mxf4nvf4, UE4M3 scales
  * per 16, FP32 accumulation in TMEM):  D[M, N] = alpha * A[M,K] . B[N,K]^T
  * with alpha = *a->scale32 * *b->scale32 (+ beta*D if accumulate).  CTA pairs

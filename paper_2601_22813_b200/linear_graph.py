@@ -21,9 +21,9 @@ from . import _lib
 from .ms_eden import msed
 from .quantizers import NVFP4Tensor, _err_word, _finish, as_device_matrix, quantize_rtn_46, stream_handle
 from .rht import CHUNK, SeedPair, derive_stream
-from .sr import rht_sr
+from .sr import SquareBlockTensor, quantize_sr, quantize_square_block, rht_sr
 
-FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16")
+FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16", "rtn_16x16", "rtn_16x16_46")
 BACKWARD_SCHEMES = ("ms_eden", "sr_rht")
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
@@ -55,7 +55,8 @@ def _keep(main: torch.cuda.Stream, *tensors) -> None:
 @dataclass(frozen=True)
 class LayerConfig:
     """linear_graph.py:73-99, restricted to the recipes this build accelerates: quartet2
-    (rtn_1x16_46 + ms_eden) and tetrajet_v2 (rtn_1x16 + sr_rht)."""
+    (rtn_1x16_46 + ms_eden), tetrajet_v2 (rtn_1x16 + sr_rht), nvidia (rtn_16x16 +
+    sr_rht, reused weights) and four_over_six (rtn_16x16_46 + sr_rht, reused weights)."""
 
     forward_scheme: str = "rtn_1x16_46"
     backward_scheme: str = "ms_eden"
@@ -70,8 +71,11 @@ class LayerConfig:
             raise ValueError(f"unknown backward scheme {self.backward_scheme!r}")
         if self.ablation != "full":
             raise ValueError(f"unknown ablation {self.ablation!r}")
-        if self.reuse_forward_weights:
-            raise ValueError("reuse_forward_weights needs the square-block forward (not built)")
+        if self.reuse_forward_weights and self.backward_scheme == "ms_eden":
+            raise ValueError("ms_eden requires weight re-quantization")
+        if self.reuse_forward_weights and not self.forward_scheme.startswith("rtn_16x16"):
+            # the reused 1x16 W^T is a dense (unquantized) GEMM operand in the reference
+            raise ValueError("reuse_forward_weights is built for the square-block weights only")
 
 
 def baseline_config(name: str) -> LayerConfig:
@@ -80,7 +84,11 @@ def baseline_config(name: str) -> LayerConfig:
         return LayerConfig()
     if name == "tetrajet_v2":
         return LayerConfig("rtn_1x16", "sr_rht")
-    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2']")
+    if name == "nvidia":
+        return LayerConfig("rtn_16x16", "sr_rht", reuse_forward_weights=True)
+    if name == "four_over_six":
+        return LayerConfig("rtn_16x16_46", "sr_rht", reuse_forward_weights=True)
+    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2', 'nvidia', 'four_over_six']")
 
 
 @dataclass
@@ -88,7 +96,7 @@ class LinearTape:
     """Quantized forward operands saved for the backward pass (linear_graph.py:102-110)."""
 
     qX: NVFP4Tensor
-    qW: NVFP4Tensor
+    qW: "NVFP4Tensor | SquareBlockTensor"
     x_shape: tuple
     w_shape: tuple
     config: LayerConfig
@@ -157,11 +165,16 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     side = _side_stream(x2.device)
     side.wait_stream(main)
     with torch.cuda.stream(side):
-        qw = quantize_rtn_46(w2, caps, _err=err)
+        if cfg.forward_scheme.startswith("rtn_16x16"):                     # linear_graph.py:214-221
+            qw = quantize_square_block(w2, len(caps) == 2, _err=err)
+        else:
+            qw = quantize_rtn_46(w2, caps, _err=err)
     qx = quantize_rtn_46(x2, caps, _err=err)
     main.wait_stream(side)
-    _keep(main, qw)
-    y = gemm(qx, qw, out_dtype)
+    wop = qw.rows if isinstance(qw, SquareBlockTensor) else qw
+    for t in ((qw.rows, qw.t) if isinstance(qw, SquareBlockTensor) else (qw,)):
+        _keep(main, t)
+    y = gemm(qx, wop, out_dtype)
     if own:
         _finish(err)
     return y, LinearTape(qx, qw, xs, ws, cfg)
@@ -195,8 +208,14 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         qxt = quant(tape.qX, PAIR_DW, 1, "tape")
         dw = gemm(qet, qxt, torch.float32)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
-    qe = quant(e2, PAIR_DX, 0, "rows")
-    qwt = quant(tape.qW, PAIR_DX, 1, "tape")
+    qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
+    if cfg.reuse_forward_weights:
+        # saved square-block W^T goes in as is; E alone, SR without rotation (linear_graph.py:308-314)
+        qe = quantize_sr(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err)
+        qwt = tape.qW.t
+    else:
+        qe = quant(e2, PAIR_DX, 0, "rows")
+        qwt = quant(qw, PAIR_DX, 1, "tape")
     dx = gemm(qe, qwt, dx_dtype)
     main.wait_stream(side)
     _keep(main, dw)

@@ -222,6 +222,8 @@ def quantize_rtn(x, s=FP4_ABS_MAX, _err=None) -> NVFP4Tensor:
 
 def dequantize(t: NVFP4Tensor) -> torch.Tensor:
     """Reconstruct the real-valued tensor, float64 on device (quantizers.py:315-323)."""
+    if hasattr(t, "rows") and isinstance(t.rows, NVFP4Tensor):     # SquareBlockTensor: expanded block scales
+        t = t.rows
     if not isinstance(t, NVFP4Tensor):
         raise TypeError(f"cannot dequantize {type(t).__name__}")
     out = torch.empty((t.R, t.K), dtype=torch.float64, device=t.device)

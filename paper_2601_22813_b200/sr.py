@@ -1,5 +1,6 @@
-"""Stochastic-rounding NVFP4 baselines (host mirror of quantizers.py:139-161,
-:237-262 and linear_graph._sr_pair, linear_graph.py:259-274).
+"""Baseline-recipe quantizers: stochastic rounding (host mirror of
+quantizers.py:139-161, :237-262 and linear_graph._sr_pair, linear_graph.py:259-274)
+and 16x16 square blocks (quantizers.py:102-111, :265-312).
 
 ``quantize_sr`` / ``quantize_sr_46`` keep the reference's signatures.  ``rht_sr``
 is one operand of the ``sr_rht`` backward scheme (the tetrajet_v2 recipe):
@@ -102,3 +103,53 @@ def rht_sr(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "row
     if own:
         _finish(err)
     return out
+
+
+class SquareBlockTensor:
+    """quantizers.py:102-111: codes [R, C], one E4M3 scale per 16x16 block.
+
+    Held in HBM twice for the GEMMs -- ``rows`` ([R, C], the forward weight
+    operand) and ``t`` (its transpose [C, R], the reused dX operand) -- each with
+    the block scale expanded into the per-16 layout, plus the compact block
+    scales ``s8`` [R/16, C/16].  ``to_reference()`` gives (fp4, scales8, scale32).
+    """
+
+    def __init__(self, rows: NVFP4Tensor, t: NVFP4Tensor, s8: torch.Tensor):
+        self.rows, self.t, self.s8 = rows, t, s8
+
+    @property
+    def shape(self):
+        return self.rows.shape
+
+    @property
+    def device(self):
+        return self.rows.device
+
+    @property
+    def scale32(self):
+        return self.rows.scale32
+
+    def to_reference(self):
+        fp4, _, s32 = self.rows.to_reference()
+        return fp4, self.s8.cpu().numpy(), s32
+
+
+def quantize_square_block(x, use_46: bool = False, _err=None) -> SquareBlockTensor:
+    """One E4M3 scale per 16x16 block, cap 256; 6/4 per block with use_46 (quantizers.py:265-312)."""
+    x2, shape, dt = as_device_matrix(x)
+    if len(shape) != 2 or shape[0] % GROUP or shape[1] % GROUP:
+        raise ValueError("square-block input must be 2D with both dims multiples of 16")
+    R, C = x2.shape
+    rows, t = NVFP4Tensor.empty((R, C), x2.device), NVFP4Tensor.empty((C, R), x2.device)
+    s8 = torch.empty((R // GROUP, C // GROUP), dtype=torch.uint8, device=x2.device)
+    own = _err is None
+    err = _err_word(x2.device) if own else _err
+    L = _lib.lib()
+    ws = torch.empty(16, dtype=torch.uint8, device=x2.device)
+    rc_, tc_ = rows.c(), t.c()
+    _lib.check(L.q2_quant_square_block(x2.data_ptr(), dt, R, C, int(bool(use_46)), ctypes.byref(rc_), ctypes.byref(tc_),
+                                       s8.data_ptr(), ws.data_ptr(), err.data_ptr(), stream_handle()),
+               "quantize_square_block")
+    if own:
+        _finish(err)
+    return SquareBlockTensor(rows, t, s8)

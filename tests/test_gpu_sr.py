@@ -87,3 +87,46 @@ def test_tetrajet_v2_linear(cuda):
         got = got.double().cpu().numpy()
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("use_46", [False, True])
+def test_quantize_square_block(cuda, family, use_46):
+    """16x16 blocks (quantizers.py:265-312): codes, block scales, scale32; the transposed
+    copy holds the same codes and the same (expanded) block scales."""
+    q2 = _q2()
+    x = make(family, (96, 160), seed=16)
+    t = q2.quantize_square_block(_dev(x), use_46)
+    ref = O.quantize_square_block(x, use_46)
+    fp4, s8, s32 = t.to_reference()
+    assert np.float32(s32).tobytes() == np.float32(ref.scale32).tobytes()
+    np.testing.assert_array_equal(s8, ref.scales8)
+    np.testing.assert_array_equal(fp4, ref.fp4)
+    tf, ts, _ = t.t.to_reference()
+    np.testing.assert_array_equal(tf, ref.fp4.T)
+    np.testing.assert_array_equal(ts, np.repeat(ref.scales8.T, 16, axis=0))
+    one_col = make(family, (64, 16), seed=17)                           # single block column: flat sum order
+    got = q2.quantize_square_block(_dev(one_col), use_46).to_reference()
+    ref = O.quantize_square_block(one_col, use_46)
+    np.testing.assert_array_equal(got[0], ref.fp4)
+    np.testing.assert_array_equal(got[1], ref.scales8)
+
+
+@pytest.mark.parametrize("name,fwd", [("nvidia", "rtn_16x16"), ("four_over_six", "rtn_16x16_46")])
+def test_square_block_recipes_linear(cuda, name, fwd):
+    """nvidia / four_over_six: square-block W, reused W^T in dX, sr_rht dW (linear_graph.py:119-140, :308-326)."""
+    q2 = _q2()
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.baseline_config(name)
+    y, tape = q2.forward(_dev(x), _dev(w), cfg)
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9))
+    ry, rtape = O.forward(x, w, forward_scheme=fwd)
+    assert_same(tape.qX, rtape[0], "qX")
+    np.testing.assert_array_equal(tape.qW.to_reference()[0], rtape[1].fp4)
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), backward_scheme="sr_rht", reuse_forward_weights=True)
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        got = got.double().cpu().numpy()
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 1e-5, rel

@@ -72,12 +72,19 @@ def test_sf_layout_formula():
 def test_layer_config_validation():
     import paper_2601_22813_b200 as q2
     with pytest.raises(ValueError):
-        q2.LayerConfig(forward_scheme="rtn_16x16")
+        q2.LayerConfig(forward_scheme="rtn_32x32")
     with pytest.raises(ValueError):
-        q2.LayerConfig(reuse_forward_weights=True)
+        q2.LayerConfig(reuse_forward_weights=True)                  # ms_eden re-quantizes W
     with pytest.raises(ValueError):
-        q2.baseline_config("nvidia")
+        q2.LayerConfig("rtn_1x16", "sr_rht", reuse_forward_weights=True)   # dense reused W^T: not built
+    with pytest.raises(ValueError):
+        q2.LayerConfig(backward_scheme="sr_46")
+    with pytest.raises(ValueError):
+        q2.baseline_config("four_over_six_backward")
     assert q2.baseline_config("quartet2") == q2.LayerConfig()
+    assert q2.baseline_config("tetrajet_v2") == q2.LayerConfig("rtn_1x16", "sr_rht")
+    assert q2.baseline_config("nvidia") == q2.LayerConfig("rtn_16x16", "sr_rht", reuse_forward_weights=True)
+    assert q2.baseline_config("four_over_six").forward_scheme == "rtn_16x16_46"
 
 
 def test_constants_match_reference_arithmetic():
