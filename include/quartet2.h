@@ -159,6 +159,13 @@ int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const 
  *   x_rot = rht_apply(x, sign_mask) along K (rht.py:144-155), then quantize_sr
  *   of x_rot with the same constants; sources as q2_msed_quant.  Two passes
  *   over x (absmax of x_rot, then quantize).  ws: q2_msed_ws_bytes(R, K).    */
+/*   q2_sr_quant_src: the general SR operand quantizer of _sr_pair: rotate 0/1
+ *   (sr / sr_46 vs sr_rht / sr_rht_46), ncaps 1 (quantize_sr) or 2
+ *   (quantize_sr_46 with branch streams stream0, stream1), any source.       */
+int q2_sr_quant_src(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K, int64_t ld,
+                    int rotate, const uint32_t sign_mask[4], int ncaps, double cap0, double cap1, double margin,
+                    double scale_div, double inv_sqrt_chunk, uint64_t seed, uint64_t stream0, uint64_t stream1,
+                    const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);
 size_t q2_quant_sr_ws_bytes(void);
 int q2_quant_sr(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0, double cap1,
                 double margin, double scale_div, uint64_t seed, uint64_t stream0, uint64_t stream1,

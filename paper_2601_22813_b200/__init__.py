@@ -11,7 +11,7 @@ from .quantizers import (GROUP, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, 
 from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
                       pass1, pass2,
                       posthoc_quantize)
-from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr
+from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr, sr_operand
 from .linear_graph import (GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config, forward,
                            gemm, gemm_emulated)
 
@@ -21,5 +21,5 @@ __all__ = [
     "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual_posthoc", "pass1", "pass2", "posthoc_quantize",
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
-    "quantize_sr", "quantize_sr_46", "rht_sr", "quantize_square_block", "SquareBlockTensor",
+    "quantize_sr", "quantize_sr_46", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
 ]

@@ -131,6 +131,8 @@ static M64Args base_args(const M64Src& s, int64_t R, int64_t K, const uint32_t s
   a.tiles_r = (int)((R + M64_ROWS - 1) / M64_ROWS);
   a.tiles_c = (int)(K / CHUNK);
   a.fc = FastDiv((uint32_t)a.tiles_c);
+  a.rotate = 1;
+  a.sr_ncaps = 1;
   return a;
 }
 
@@ -184,26 +186,39 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   return dispatch_m64<M64_QUANT>(src, a, st);
 }
 
-extern "C" int q2_rht_sr_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K,
-                               int64_t ld, const uint32_t sign_mask[4], double cap, double margin, double scale_div,
-                               double inv_sqrt_chunk, uint64_t seed, uint64_t sr_stream, const q2_nvfp4* out,
-                               void* ws, uint32_t* err, void* stream) {
-  if (!out || !ws || !sign_mask || out->R != R || out->K != K) return Q2_EINVAL;
+extern "C" int q2_sr_quant_src(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K,
+                               int64_t ld, int rotate, const uint32_t sign_mask[4], int ncaps, double cap0,
+                               double cap1, double margin, double scale_div, double inv_sqrt_chunk, uint64_t seed,
+                               uint64_t stream0, uint64_t stream1, const q2_nvfp4* out, void* ws, uint32_t* err,
+                               void* stream) {
+  if (!out || !ws || !sign_mask || out->R != R || out->K != K || (ncaps != 1 && ncaps != 2)) return Q2_EINVAL;
   const M64Src src{x, dtype, ld, tape, src_kind};
   int rc = check_src(src, R, K);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
-  M64Args a = base_args(src, R, K, sign_mask, cap, inv_sqrt_chunk);
+  const uint32_t none[4] = {0u, 0u, 0u, 0u};
+  M64Args a = base_args(src, R, K, rotate ? sign_mask : none, cap0, inv_sqrt_chunk);
+  a.rotate = rotate ? 1 : 0;
   a.red = reinterpret_cast<unsigned long long*>(w);
   a.err = err;
   a.codes = out->codes; a.sf = out->sf; a.scale32 = out->scale32;
-  a.sr_head = prng_head(seed, sr_stream);
+  a.sr_head = prng_head(seed, stream0);
+  a.sr_head1 = prng_head(seed, stream1);
+  a.sr_ncaps = ncaps; a.sr_cap1 = cap1;
   a.sr_div = scale_div; a.sr_margin = margin;
   if (cudaMemsetAsync(w, 0, 16, st) != cudaSuccess) return Q2_ECUDA;
   if (R == 0 || K == 0) return cudaMemsetAsync(out->scale32, 0, 4, st) == cudaSuccess ? Q2_OK : Q2_ECUDA;
   if ((rc = dispatch_m64<M64_ABSMAX>(src, a, st))) return rc;
   return dispatch_m64<M64_SR>(src, a, st);
+}
+
+extern "C" int q2_rht_sr_quant(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R, int64_t K,
+                               int64_t ld, const uint32_t sign_mask[4], double cap, double margin, double scale_div,
+                               double inv_sqrt_chunk, uint64_t seed, uint64_t sr_stream, const q2_nvfp4* out,
+                               void* ws, uint32_t* err, void* stream) {
+  return q2_sr_quant_src(x, dtype, tape, src_kind, R, K, ld, 1, sign_mask, 1, cap, 0.0, margin, scale_div,
+                         inv_sqrt_chunk, seed, sr_stream, 0, out, ws, err, stream);
 }
 
 extern "C" int q2_posthoc_pass1(const void* x, int dtype, const q2_nvfp4* tape, int src_kind, int64_t R,

@@ -55,6 +55,10 @@ struct M64Args {
   int tiles_r, tiles_c;
   FastDiv fc;                                     // division by tiles_c
   double sr_div, sr_margin;                       // M64_SR: scale32 = amax / sr_div, D = (scale32 * s) * sr_margin
+  double sr_cap1;                                 // M64_SR, 4/6: the second ceiling (branch stream head sr_head1)
+  int sr_ncaps;                                   // M64_SR: 1 = quantize_sr, 2 = quantize_sr_46
+  uint64_t sr_head1;
+  int rotate;                                     // 0: no Hadamard rotation (plain SR schemes)
 };
 
 template <int SRC, int DT>
@@ -252,12 +256,13 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   float scale32 = 0.f;
   bool zero = false;                                 // all-zero tensor (quantizers.py:175-176)
   double sdiv = a.s;                                 // gmax / sdiv -> scale candidate
-  double sr_d = 0.0;                                 // M64_SR: the group-scale divisor (scale32 * cap) * margin
+  double sr_d = 0.0, sr_d1 = 0.0;                     // M64_SR: group-scale divisors (scale32 * cap_b) * margin
   if (MODE == M64_SR) {
     const double amax = bitsd(a.red[0]);
     zero = amax == 0.0;
     scale32 = zero ? 0.f : __double2float_rn(__ddiv_rn(amax, a.sr_div));
     sr_d = __dmul_rn(__dmul_rn((double)scale32, a.s), a.sr_margin);
+    sr_d1 = __dmul_rn(__dmul_rn((double)scale32, a.sr_cap1), a.sr_margin);
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.scale32 = scale32;
   }
   if (MODE == M64_QUANT) {
@@ -280,6 +285,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   const float isd_lo = __frcp_rd(__double2float_ru(sdiv)), isd_hi = __frcp_ru(__double2float_rd(sdiv));
   const int64_t gpr = a.K / GROUP;
   const double c_eff = a.inv_sqrt;
+  const bool rot = (MODE == M64_SR || MODE == M64_ABSMAX) ? a.rotate != 0 : true;
   uint64_t wabs = 0, wp = 0;                          // running |y| max / pseudo max (f64 bits)
   bool bad = false, ovf = false, nanscale = false;
 
@@ -354,6 +360,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       // fl64(FWHT(x * scale32) * c) (all of its float64 partial sums are exact too).
       const int* sp = reinterpret_cast<const int*>(smem + TL::OFF_SPAN) + 16 * (it % 3) + 2 * (warp >> 1);
       fwht_done = sp[1] - sp[0] <= 7;                          // warp-uniform (one group per warp)
+      if (!rot) fwht_done = false;                             // unrotated: y = dequantized value
       float z[16][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -446,7 +453,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
 
     // ---------------------------------------------------------------- FWHT
-    if (!fwht_done) {
+    if (!fwht_done && rot) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {                   // h = 1 (bit b)
       const double u = y[k][0], v = y[k][1];
@@ -514,25 +521,53 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       }
       uint32_t cw[4] = {0u, 0u, 0u, 0u}, sbw = 0;
       const uint64_t ibase = (uint64_t)r * (uint64_t)a.K + (uint64_t)tc * CHUNK + 2 * q;
+      const int quad = lane & ~3;
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
-        if (gm[g] >= 0x7FF0000000000000ull) { if (live) bad = true; continue; }
-        const double gmax = bitsd(gm[g]);
-        const uint32_t sb = zero ? 0u : e4m3_rtn(__ddiv_rn(gmax, sr_d));
-        const double dg = __dmul_rn(e4m3_val(sb), (double)scale32);
-        if (live && dg > 0.0 && __ddiv_rn(gmax, dg) > 6.0 * (1.0 + 1e-9)) ovf = true;   // non-clipping check
-        if (g == 2 * q) sbw |= sb;
-        if (g == 2 * q + 1) sbw |= sb << 8;
+        const bool fin = gm[g] < 0x7FF0000000000000ull;       // quad-uniform; no early exit (shuffles below)
+        if (!fin && live) bad = true;
+        const double gmax = fin ? bitsd(gm[g]) : 0.0;
+        uint32_t sbest = 0, cbest[2] = {0u, 0u};              // codes of k = 2g, 2g+1 (byte: b0 | b1 << 4)
+        double ebest = 0.0;
+        for (int br = 0; br < a.sr_ncaps; ++br) {
+          const double dsr = br ? sr_d1 : sr_d;
+          const uint32_t sb = zero ? 0u : e4m3_rtn(__ddiv_rn(gmax, dsr));
+          const double dg = __dmul_rn(e4m3_val(sb), (double)scale32);
+          // non-clipping check of quantize_sr (quantizers.py:153-157); not in the 4/6 variant
+          if (a.sr_ncaps == 1 && live && dg > 0.0 && __ddiv_rn(gmax, dg) > 6.0 * (1.0 + 1e-9)) ovf = true;
+          const uint64_t head = br ? a.sr_head1 : a.sr_head;
+          uint32_t cc[2] = {0u, 0u};
+          double sq[2][2];
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int k = 2 * g + kk;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const uint64_t u53 = mix64(head ^ (ibase + 8 * k + b + GOLDEN)) >> 11;
+              double dq = 0.0;
+              const uint32_t c = zero ? 0u : sr_elem(y[k][b], dg, u53, &dq);
+              cc[kk] |= c << (4 * b);
+              const double df = __dsub_rn(dq, y[k][b]);
+              sq[kk][b] = __dmul_rn(df, df);
+            }
+          }
+          double e = 0.0;
+          if (a.sr_ncaps == 2) {                                 // sequential float64 error, element order
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) e = __dadd_rn(e, __shfl_sync(0xFFFFFFFFu, sq[kk][b], quad + qq));
+          }
+          if (br == 0 || e < ebest) { ebest = e; sbest = sb; cbest[0] = cc[0]; cbest[1] = cc[1]; }
+        }
+        if (g == 2 * q) sbw |= sbest;
+        if (g == 2 * q + 1) sbw |= sbest << 8;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const int k = 2 * g + kk;
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const uint64_t u53 = mix64(a.sr_head ^ (ibase + 8 * k + b + GOLDEN)) >> 11;
-            double dq;
-            const uint32_t c = zero ? 0u : sr_elem(y[k][b], dg, u53, &dq);
-            cw[k >> 2] |= c << (8 * (k & 3) + 4 * b);
-          }
+          cw[k >> 2] |= cbest[kk] << (8 * (k & 3));
         }
       }
       const uint32_t cst = smem_u32(smem + TL::OFF_CST + warp * 640) + rw * 80;

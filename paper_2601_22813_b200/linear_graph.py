@@ -21,10 +21,10 @@ from . import _lib
 from .ms_eden import msed
 from .quantizers import NVFP4Tensor, _err_word, _finish, as_device_matrix, quantize_rtn_46, stream_handle
 from .rht import CHUNK, SeedPair, derive_stream
-from .sr import SquareBlockTensor, quantize_sr, quantize_square_block, rht_sr
+from .sr import SquareBlockTensor, quantize_sr, quantize_sr_46, quantize_square_block, sr_operand
 
 FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16", "rtn_16x16", "rtn_16x16_46")
-BACKWARD_SCHEMES = ("ms_eden", "sr_rht")
+BACKWARD_SCHEMES = ("ms_eden", "sr_rht", "sr", "sr_46", "sr_rht_46")
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
 
@@ -88,7 +88,10 @@ def baseline_config(name: str) -> LayerConfig:
         return LayerConfig("rtn_16x16", "sr_rht", reuse_forward_weights=True)
     if name == "four_over_six":
         return LayerConfig("rtn_16x16_46", "sr_rht", reuse_forward_weights=True)
-    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2', 'nvidia', 'four_over_six']")
+    if name == "four_over_six_backward":
+        return LayerConfig("rtn_16x16_46", "sr_46", reuse_forward_weights=True)
+    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2', 'nvidia', 'four_over_six', "
+                     f"'four_over_six_backward']")
 
 
 @dataclass
@@ -197,9 +200,12 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     side = _side_stream(e2.device)
     side.wait_stream(main)
     # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
-    if cfg.backward_scheme == "sr_rht":                 # linear_graph.py:259-274 via :310-326
+    sr_46 = cfg.backward_scheme in ("sr_46", "sr_rht_46")
+    if cfg.backward_scheme != "ms_eden":                # _sr_pair, linear_graph.py:259-274 via :310-326
+        rotate = cfg.backward_scheme in ("sr_rht", "sr_rht_46")
+
         def quant(x, pair, operand, source):
-            return rht_sr(x, seeds, derive_stream(pair, operand), pair, source, err)
+            return sr_operand(x, seeds, derive_stream(pair, operand), pair, source, rotate, sr_46, err)
     else:                                               # ms_eden, linear_graph.py:304-307, :322-326
         def quant(x, pair, operand, source):
             return msed(x, seeds, 6.0, derive_stream(pair, operand), pair, mode, source, err)
@@ -211,7 +217,7 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
     if cfg.reuse_forward_weights:
         # saved square-block W^T goes in as is; E alone, SR without rotation (linear_graph.py:308-314)
-        qe = quantize_sr(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err)
+        qe = (quantize_sr_46 if sr_46 else quantize_sr)(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err)
         qwt = tape.qW.t
     else:
         qe = quant(e2, PAIR_DX, 0, "rows")

@@ -60,8 +60,10 @@ def quantize_sr_46(x, seed, stream=0, caps=(6.0, 4.0), _err=None) -> NVFP4Tensor
     return _sr(x, seed, (derive_stream(stream, 0), derive_stream(stream, 1)), caps, caps[0] * GUARDED_SCALE_CAP, _err)
 
 
-def rht_sr(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "rows", err=None) -> NVFP4Tensor:
-    """quantize_sr(rht_apply(x, seeds.rht, rotation_id), seeds.sr, stream) of a logical [R, K] tensor.
+def sr_operand(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "rows", rotate: bool = True,
+               use_46: bool = False, err=None) -> NVFP4Tensor:
+    """One operand of an SR backward scheme (_sr_pair, linear_graph.py:259-274) of a logical [R, K] tensor:
+    quantize_sr / quantize_sr_46 (use_46) of x, or of rht_apply(x, seeds.rht, rotation_id) (rotate).
 
     source="rows": x is [R, K]; "cols": x is [K, R] (quantizes x^T); "tape": x
     is an NVFP4Tensor [K, R] (quantizes dequant(x)^T).
@@ -88,7 +90,8 @@ def rht_sr(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "row
             raise ValueError(f"unknown source {source!r}")
         xp, ld = x2.data_ptr(), x2.shape[1]
     if K % CHUNK:
-        raise ValueError(f"rotation requires the last dimension ({K}) to be a multiple of {CHUNK}")  # rht.py:147-150
+        # rht.py:147-150 for the rotation; this build's transposed sources tile K by 128 as well
+        raise ValueError(f"rotation requires the last dimension ({K}) to be a multiple of {CHUNK}")
     out = NVFP4Tensor.empty((R, K), dev)
     own = err is None
     if own:
@@ -96,13 +99,23 @@ def rht_sr(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "row
     ws = torch.empty(L.q2_msed_ws_bytes(R, K), dtype=torch.uint8, device=dev)
     oc = out.c()
     mask = _lib._U32x4(*sign_mask(int(seeds.rht), int(rotation_id)))
-    rc = L.q2_rht_sr_quant(xp, dt, ctypes.byref(tape_c) if tape_c is not None else None, src, R, K, ld, mask,
-                           FP4_ABS_MAX, FP8_RTN_MARGIN, _SR_SCALE_DIV, INV_SQRT_CHUNK, int(seeds.sr) & _M64,
-                           int(stream) & _M64, ctypes.byref(oc), ws.data_ptr(), err.data_ptr(), stream_handle())
-    _lib.check(rc, "rht_sr")
+    if use_46:                                            # quantizers.py:237-262
+        caps, div, streams = (6.0, 4.0), 6.0 * GUARDED_SCALE_CAP, (derive_stream(stream, 0), derive_stream(stream, 1))
+    else:                                                 # quantizers.py:139-161
+        caps, div, streams = (FP4_ABS_MAX, 0.0), _SR_SCALE_DIV, (stream, 0)
+    rc = L.q2_sr_quant_src(xp, dt, ctypes.byref(tape_c) if tape_c is not None else None, src, R, K, ld,
+                           int(bool(rotate)), mask, 2 if use_46 else 1, caps[0], caps[1], FP8_RTN_MARGIN, div,
+                           INV_SQRT_CHUNK, int(seeds.sr) & _M64, int(streams[0]) & _M64, int(streams[1]) & _M64,
+                           ctypes.byref(oc), ws.data_ptr(), err.data_ptr(), stream_handle())
+    _lib.check(rc, "sr_operand")
     if own:
         _finish(err)
     return out
+
+
+def rht_sr(x, seeds: SeedPair, stream: int, rotation_id: int, source: str = "rows", err=None) -> NVFP4Tensor:
+    """quantize_sr(rht_apply(x, seeds.rht, rotation_id), seeds.sr, stream): one sr_rht operand."""
+    return sr_operand(x, seeds, stream, rotation_id, source, True, False, err)
 
 
 class SquareBlockTensor:

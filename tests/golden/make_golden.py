@@ -66,7 +66,7 @@ def main():
     y, tape = LG.forward(X, W, LG.baseline_config("tetrajet_v2"))
     g = LG.backward(tape, E, RH.SeedPair(7, 9))
     out.update(tj_Y=y, tj_dX=g.dX, tj_dW=g.dW)
-    for name, tag in (("nvidia", "nv"), ("four_over_six", "fos")):
+    for name, tag in (("nvidia", "nv"), ("four_over_six", "fos"), ("four_over_six_backward", "fosb")):
         y, tape = LG.forward(X, W, LG.baseline_config(name))
         g = LG.backward(tape, E, RH.SeedPair(7, 9))
         out.update({f"{tag}_Y": y, f"{tag}_dX": g.dX, f"{tag}_dW": g.dW})

@@ -130,3 +130,42 @@ def test_square_block_recipes_linear(cuda, name, fwd):
         got = got.double().cpu().numpy()
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("rotate,use_46", [(False, False), (False, True), (True, True)])
+@pytest.mark.parametrize("source", ["rows", "cols", "tape"])
+def test_sr_operand(cuda, source, rotate, use_46):
+    """The general _sr_pair operand: plain / rotated, quantize_sr / quantize_sr_46, every source."""
+    q2 = _q2()
+    seeds = q2.SeedPair(21, 23)
+    x = make("normal", (256, 384), seed=18)
+    if source == "tape":
+        qx = q2.quantize_rtn_46(_dev(x), caps=(6.0,))
+        gpu_fn = lambda: q2.sr_operand(qx, seeds, 55, 8, "tape", rotate, use_46)     # noqa: E731
+        logical = np.ascontiguousarray(O.dequantize(O.quantize_rtn_46(x, caps=(6.0,))).T)
+    else:
+        gpu_fn = lambda: q2.sr_operand(_dev(x), seeds, 55, 8, source, rotate, use_46)  # noqa: E731
+        logical = x if source == "rows" else np.ascontiguousarray(x.T)
+    src = O.rht_apply(logical, 21, 8) if rotate else logical
+    quant = O.quantize_sr_46 if use_46 else O.quantize_sr
+    _raises_or_same(gpu_fn, lambda: quant(src, 23, 55), f"sr_operand {source} rot={rotate} 46={use_46}")
+
+
+@pytest.mark.parametrize("cfg_args,reuse", [(("rtn_1x16", "sr"), False), (("rtn_1x16", "sr_46"), False),
+                                            (("rtn_1x16_46", "sr_rht_46"), False),
+                                            (("rtn_16x16_46", "sr_46"), True)])
+def test_sr_schemes_linear(cuda, cfg_args, reuse):
+    """Every SR backward scheme of linear_graph.backward (:290-326), incl. four_over_six_backward."""
+    q2 = _q2()
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.LayerConfig(*cfg_args, reuse_forward_weights=reuse)
+    y, tape = q2.forward(_dev(x), _dev(w), cfg)
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9))
+    ry, rtape = O.forward(x, w, forward_scheme=cfg_args[0])
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), backward_scheme=cfg_args[1], reuse_forward_weights=reuse)
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        got = got.double().cpu().numpy()
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 1e-5, rel

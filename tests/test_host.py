@@ -78,9 +78,10 @@ def test_layer_config_validation():
     with pytest.raises(ValueError):
         q2.LayerConfig("rtn_1x16", "sr_rht", reuse_forward_weights=True)   # dense reused W^T: not built
     with pytest.raises(ValueError):
-        q2.LayerConfig(backward_scheme="sr_46")
+        q2.LayerConfig(backward_scheme="sr_rtn")
     with pytest.raises(ValueError):
-        q2.baseline_config("four_over_six_backward")
+        q2.baseline_config("identity")
+    assert q2.baseline_config("four_over_six_backward").backward_scheme == "sr_46"
     assert q2.baseline_config("quartet2") == q2.LayerConfig()
     assert q2.baseline_config("tetrajet_v2") == q2.LayerConfig("rtn_1x16", "sr_rht")
     assert q2.baseline_config("nvidia") == q2.LayerConfig("rtn_16x16", "sr_rht", reuse_forward_weights=True)
