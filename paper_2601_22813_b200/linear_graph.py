@@ -19,12 +19,13 @@ import torch
 
 from . import _lib
 from .ms_eden import msed
-from .quantizers import NVFP4Tensor, _err_word, _finish, as_device_matrix, quantize_rtn_46, stream_handle
+from .quantizers import (NVFP4Tensor, _err_word, _finish, as_device_matrix, dequantize, quantize_rtn_46,
+                         stream_handle)
 from .rht import CHUNK, SeedPair, derive_stream
 from .sr import SquareBlockTensor, quantize_sr, quantize_sr_46, quantize_square_block, sr_operand
 
-FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16", "rtn_16x16", "rtn_16x16_46")
-BACKWARD_SCHEMES = ("ms_eden", "sr_rht", "sr", "sr_46", "sr_rht_46")
+FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16", "rtn_16x16", "rtn_16x16_46", "identity")
+BACKWARD_SCHEMES = ("ms_eden", "sr_rht", "sr", "sr_46", "sr_rht_46", "identity")
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
 
@@ -90,8 +91,10 @@ def baseline_config(name: str) -> LayerConfig:
         return LayerConfig("rtn_16x16_46", "sr_rht", reuse_forward_weights=True)
     if name == "four_over_six_backward":
         return LayerConfig("rtn_16x16_46", "sr_46", reuse_forward_weights=True)
+    if name == "identity":
+        return LayerConfig("identity", "identity")
     raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2', 'nvidia', 'four_over_six', "
-                     f"'four_over_six_backward']")
+                     f"'four_over_six_backward', 'identity']")
 
 
 @dataclass
@@ -143,8 +146,10 @@ def _check_dims(x_shape, w_shape, cfg: LayerConfig) -> None:
     out_dim, w_in = w_shape
     if w_in != in_dim:
         raise ValueError(f"X is {x_shape} but W is {w_shape}")
-    if in_dim % 16:
+    if cfg.forward_scheme != "identity" and in_dim % 16:
         raise ValueError("in dimension must be a multiple of 16")
+    if cfg.backward_scheme == "identity":
+        return
     in_div = CHUNK if cfg.backward_scheme == "ms_eden" else 16
     if in_dim % in_div or out_dim % CHUNK or tokens % CHUNK:
         raise ValueError(
@@ -161,6 +166,9 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     w2, ws, _ = as_device_matrix(w, "W")
     _check_dims(xs, ws, cfg)
     caps = (6.0, 4.0) if cfg.forward_scheme.endswith("_46") else (6.0,)   # linear_graph.py:208-221
+    if cfg.forward_scheme == "identity":              # unquantized: plain FP32 GEMM (cuBLAS), linear_graph.py:208-210
+        y = torch.matmul(x2.float(), w2.float().t()).to(out_dtype)
+        return y, LinearTape(x2, w2, xs, ws, cfg)
     own = err is None
     if own:
         err = _err_word(x2.device)
@@ -193,6 +201,10 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     if es != (tokens, out_dim):
         raise ValueError(f"E has shape {es}, expected {(tokens, out_dim)}")
     mode = "posthoc" if cfg.posthoc else "exact"
+    dense = lambda t: t.float() if isinstance(t, torch.Tensor) else dequantize(t).float()   # noqa: E731
+    if cfg.backward_scheme == "identity":             # no backward quantization (linear_graph.py:286-288)
+        ef = e2.float()
+        return GradPair(torch.matmul(ef, dense(tape.qW)).to(dx_dtype), torch.matmul(ef.t(), dense(tape.qX)))
     own = err is None
     if own:
         err = _err_word(e2.device)
@@ -211,7 +223,7 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
             return msed(x, seeds, 6.0, derive_stream(pair, operand), pair, mode, source, err)
     with torch.cuda.stream(side):
         qet = quant(e2, PAIR_DW, 0, "cols")
-        qxt = quant(tape.qX, PAIR_DW, 1, "tape")
+        qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape")
         dw = gemm(qet, qxt, torch.float32)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
     qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
@@ -221,7 +233,7 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         qwt = tape.qW.t
     else:
         qe = quant(e2, PAIR_DX, 0, "rows")
-        qwt = quant(qw, PAIR_DX, 1, "tape")
+        qwt = quant(qw, PAIR_DX, 1, "cols" if isinstance(qw, torch.Tensor) else "tape")
     dx = gemm(qe, qwt, dx_dtype)
     main.wait_stream(side)
     _keep(main, dw)

@@ -169,3 +169,22 @@ def test_sr_schemes_linear(cuda, cfg_args, reuse):
         got = got.double().cpu().numpy()
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("cfg_args", [("identity", "identity"), ("identity", "ms_eden"), ("rtn_1x16_46", "identity")])
+def test_identity_schemes_linear(cuda, cfg_args):
+    """The unquantized control (linear_graph.py:136-140 'identity') and its mixes: dense FP32
+    GEMMs (cuBLAS, no TF32) where nothing is quantized, dense X/W sources for a quantized backward."""
+    q2 = _q2()
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.LayerConfig(*cfg_args)
+    y, tape = q2.forward(_dev(x), _dev(w), cfg)
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9))
+    ry, rtape = O.forward(x, w, forward_scheme=cfg_args[0])
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), backward_scheme=cfg_args[1])
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        got = got.double().cpu().numpy()
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 1e-5, rel

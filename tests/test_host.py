@@ -80,7 +80,8 @@ def test_layer_config_validation():
     with pytest.raises(ValueError):
         q2.LayerConfig(backward_scheme="sr_rtn")
     with pytest.raises(ValueError):
-        q2.baseline_config("identity")
+        q2.baseline_config("quartet3")
+    assert q2.baseline_config("identity") == q2.LayerConfig("identity", "identity")
     assert q2.baseline_config("four_over_six_backward").backward_scheme == "sr_46"
     assert q2.baseline_config("quartet2") == q2.LayerConfig()
     assert q2.baseline_config("tetrajet_v2") == q2.LayerConfig("rtn_1x16", "sr_rht")
