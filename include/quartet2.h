@@ -90,6 +90,13 @@ size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K);
 int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
                  int ncaps, double cap0, double cap1, double scale_div,
                  const q2_nvfp4* out, void* ws, uint32_t* err, void* stream);
+/* q2_quant_fwd with the tensor absmax supplied by the producer of x (e.g. an
+ * RMSNorm or activation epilogue that atomicMax-es the float bits of |x|):
+ * the amax pass is skipped; `amax_bits` is device memory holding the float
+ * bits of max|x|.                                           */
+int q2_quant_fwd_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0,
+                      double cap1, double scale_div, const uint32_t* amax_bits, const q2_nvfp4* out, void* ws,
+                      uint32_t* err, void* stream);
 
 /* MS-EDEN backward quantizer (randomized 128-Hadamard + clipping RTN cap 256 +
  * per-chunk EDEN factor + stochastic E4M3 scale rounding).

@@ -6,7 +6,7 @@ meanings, computed by hand-written sm_100a CUDA in ``libquartet2.so``.
 """
 
 from .rht import CHUNK, SeedPair, derive_stream, prng_uniform, sign_mask
-from .quantizers import (GROUP, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
+from .quantizers import (GROUP, absmax, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
                          deserialize_nvfp4, quantize_rtn, quantize_rtn_46, serialize_nvfp4, set_error_mode)
 from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
                       pass1, pass2,
@@ -21,5 +21,5 @@ __all__ = [
     "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual_posthoc", "pass1", "pass2", "posthoc_quantize",
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
-    "quantize_sr", "quantize_sr_46", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
+    "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
 ]

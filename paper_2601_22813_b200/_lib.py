@@ -24,7 +24,7 @@ EXPORTS = (
     "q2_sf_bytes", "q2_version", "q2_amax", "q2_quant_fwd_ws_bytes", "q2_quant_fwd",
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
     "q2_msed_dual_posthoc", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
-    "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant", "q2_quant_square_block", "q2_sr_quant_src",
+    "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant", "q2_quant_square_block", "q2_sr_quant_src", "q2_quant_fwd_amax",
 )
 
 
@@ -49,6 +49,7 @@ _SIGS = {
     "q2_amax": (_I, [_P, _I, _I64, _I64, _I64, _P, _P, _P]),
     "q2_quant_fwd_ws_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "q2_quant_fwd": (_I, [_P, _I, _I64, _I64, _I64, _I, _D, _D, _D, _TP, _P, _P, _P]),
+    "q2_quant_fwd_amax": (_I, [_P, _I, _I64, _I64, _I64, _I, _D, _D, _D, _P, _TP, _P, _P, _P]),
     "q2_msed_ws_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "q2_msed_quant": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _U64, _U64, _I, _TP, _P, _P, _P]),
     "q2_posthoc_pass1": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _U32x4, _D, _D, _P, _P, _P, _P, _P, _P]),

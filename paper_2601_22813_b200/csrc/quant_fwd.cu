@@ -438,17 +438,18 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
 // ws: [0] amax bits, [1] fix-up count, [4..] fix-up list (one u32 per group).
 extern "C" size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K) { return 16 + 4 * (size_t)R * (size_t)(K / 16); }
 
-extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,
-                            double cap0, double cap1, double scale_div, const q2_nvfp4* out,
-                            void* ws, uint32_t* err, void* stream) {
+static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0,
+                     double cap1, double scale_div, const q2_nvfp4* out, const uint32_t* amax_in, void* ws,
+                     uint32_t* err, void* stream) {
   if (!out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  uint32_t* amax = static_cast<uint32_t*>(ws);
-  uint32_t* fix_count = amax + 1;
-  uint32_t* fix_list = amax + 4;
-  if (cudaMemsetAsync(amax, 0, 8, s) != cudaSuccess) return Q2_ECUDA;
-  int rc = q2_amax(x, dtype, R, K, ld, amax, err, stream);
+  uint32_t* amax_ws = static_cast<uint32_t*>(ws);
+  uint32_t* fix_count = amax_ws + 1;
+  uint32_t* fix_list = amax_ws + 4;
+  if (cudaMemsetAsync(amax_ws, 0, 8, s) != cudaSuccess) return Q2_ECUDA;
+  int rc = amax_in ? Q2_OK : q2_amax(x, dtype, R, K, ld, amax_ws, err, stream);
   if (rc) return rc;
+  const uint32_t* amax = amax_in ? amax_in : amax_ws;
   // The quantize pass streams contiguous rows (the host wrapper makes views contiguous).
   if (ld != K || (reinterpret_cast<uintptr_t>(x) & 15u) || K / 16 >= (1ll << 31) || R * (K / 16) >= (1ll << 31))
     return Q2_EINVAL;
@@ -478,4 +479,21 @@ extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int6
   }
   Q2_CHECK_LAUNCH();
   return Q2_OK;
+}
+
+extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,
+                            double cap0, double cap1, double scale_div, const q2_nvfp4* out,
+                            void* ws, uint32_t* err, void* stream) {
+  return quant_fwd(x, dtype, R, K, ld, ncaps, cap0, cap1, scale_div, out, nullptr, ws, err, stream);
+}
+
+// The tensor |x| max supplied by the producer of x: the amax
+// pass is skipped.  amax_bits = float bits of max |x| (non-negative floats
+// order like their bits, so a producer can atomicMax them); non-finite checks
+// are then the producer's job, as in q2_amax.
+extern "C" int q2_quant_fwd_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,
+                                 double cap0, double cap1, double scale_div, const uint32_t* amax_bits,
+                                 const q2_nvfp4* out, void* ws, uint32_t* err, void* stream) {
+  if (!amax_bits) return Q2_EINVAL;
+  return quant_fwd(x, dtype, R, K, ld, ncaps, cap0, cap1, scale_div, out, amax_bits, ws, err, stream);
 }

@@ -186,30 +186,51 @@ def _check_group_dim(shape) -> None:
         raise ValueError(f"last dimension must be a multiple of {GROUP}")  # quantizers.py:116-117
 
 
-def _quant_fwd(x, caps, scale_div, err=None) -> NVFP4Tensor:
+def _quant_fwd(x, caps, scale_div, err=None, amax=None) -> NVFP4Tensor:
     x2, shape, dt = as_device_matrix(x)
     _check_group_dim(shape)
     out = NVFP4Tensor.empty(shape, x2.device)
     own = err is None
     if own:
         err = _err_word(x2.device)
-    ws = torch.empty(_lib.lib().q2_quant_fwd_ws_bytes(x2.shape[0], x2.shape[1]), dtype=torch.uint8, device=x2.device)
+    L = _lib.lib()
+    ws = torch.empty(L.q2_quant_fwd_ws_bytes(x2.shape[0], x2.shape[1]), dtype=torch.uint8, device=x2.device)
     t = out.c()
     c1 = float(caps[1]) if len(caps) > 1 else 0.0
-    _lib.check(_lib.lib().q2_quant_fwd(x2.data_ptr(), dt, x2.shape[0], x2.shape[1], x2.shape[1], len(caps),
-                                       float(caps[0]), c1, float(scale_div), ctypes.byref(t), ws.data_ptr(),
-                                       err.data_ptr(), stream_handle()), "quant_fwd")
+    args = (x2.data_ptr(), dt, x2.shape[0], x2.shape[1], x2.shape[1], len(caps), float(caps[0]), c1, float(scale_div))
+    if amax is None:
+        rc = L.q2_quant_fwd(*args, ctypes.byref(t), ws.data_ptr(), err.data_ptr(), stream_handle())
+    else:
+        if not (isinstance(amax, torch.Tensor) and amax.is_cuda and amax.numel() == 1 and amax.dtype == torch.float32):
+            raise TypeError("amax must be a one-element float32 CUDA tensor holding max|x|")
+        rc = L.q2_quant_fwd_amax(*args, amax.data_ptr(), ctypes.byref(t), ws.data_ptr(), err.data_ptr(),
+                                 stream_handle())
+    _lib.check(rc, "quant_fwd")
     if own:
         _finish(err)
     return out
 
 
-def quantize_rtn_46(x, caps=(6.0, 4.0), scale_cap: float = GUARDED_SCALE_CAP, _err=None) -> NVFP4Tensor:
-    """Forward-pass RTN with per-group Four-over-Six ceiling choice (quantizers.py:206-234)."""
+def absmax(x) -> torch.Tensor:
+    """max|x| as a one-element float32 CUDA tensor (the value a fused producer would supply)."""
+    x2, _, dt = as_device_matrix(x)
+    out = torch.zeros(1, dtype=torch.float32, device=x2.device)
+    err = _err_word(x2.device)
+    _lib.check(_lib.lib().q2_amax(x2.data_ptr(), dt, x2.shape[0], x2.shape[1], x2.shape[1], out.data_ptr(),
+                                  err.data_ptr(), stream_handle()), "amax")
+    _finish(err)
+    return out
+
+
+def quantize_rtn_46(x, caps=(6.0, 4.0), scale_cap: float = GUARDED_SCALE_CAP, _err=None, amax=None) -> NVFP4Tensor:
+    """Forward-pass RTN with per-group Four-over-Six ceiling choice (quantizers.py:206-234).
+
+    ``amax``: optional max|x| from the producer of x (one-element float32 CUDA
+    tensor); skips the absmax pass."""
     caps = tuple(float(c) for c in caps)
     if len(caps) not in (1, 2):
         raise ValueError("caps must hold one or two grid ceilings")
-    return _quant_fwd(x, caps, caps[0] * scale_cap, _err)
+    return _quant_fwd(x, caps, caps[0] * scale_cap, _err, amax)
 
 
 def quantize_rtn(x, s=FP4_ABS_MAX, _err=None) -> NVFP4Tensor:

@@ -231,3 +231,15 @@ def test_nv4t_container(cuda, family):
     assert torch.equal(back.codes, t.codes)
     with pytest.raises(ValueError, match="magic"):
         q2.deserialize_nvfp4(b"XXXX" + blob[4:])
+
+
+@pytest.mark.parametrize("family", ["normal", "tie_grid", "lognormal_rows"])
+def test_quantize_rtn_46_producer_amax(cuda, family):
+    """The amax supplied by the producer (q2_quant_fwd_amax) gives the same tensor."""
+    q2 = _q2()
+    x = _dev(make(family, (192, 512), seed=19))
+    am = q2.absmax(x)
+    assert float(am.item()) == float(x.float().abs().max().item())
+    a, b = q2.quantize_rtn_46(x), q2.quantize_rtn_46(x, amax=am)
+    for u, v in zip(a.to_reference(), b.to_reference()):       # (sf padding rows are unspecified)
+        assert np.array_equal(np.asarray(u), np.asarray(v))
