@@ -353,8 +353,12 @@ def kernel_breakdown(q2, data, cfg, dev):
     work_per_launch = sum(x[2] for x in lst) / launches
     if "TFLOP/s" in d:
         peak = 4.0 * bf16
+        # ncu --set full of the c3 UpGate fprop and dgrad launches (profiles/r1_nvfp4_gemm_kernel_details.csv):
+        # 371.0 MB and 169.6 MB DRAM read+write -- the bf16 output dominates fprop
+        traffic = (371.0e6 + 169.6e6) / 2 if dom.startswith("nvfp4_gemm_kernel<bf16") else None
         roof = {"bound": "tensor", "kernel": dom, "achieved": d["TFLOP/s"], "peak": peak, "unit": "TFLOP/s",
-                "frac": d["TFLOP/s"] / peak, "traffic": None, "flops_per_launch": work_per_launch,
+                "frac": d["TFLOP/s"] / peak, "traffic": traffic, "flops_per_launch": work_per_launch,
+                "traffic_note": "bytes per launch, mean of the UpGate fprop and dgrad ncu captures",
                 "ms_per_launch": ms_of[dom] / launches,
                 "peak_source": f"4 x bf16_tflops of {src} (dense NVFP4:BF16 = 4:1 on B200; nominal 9 PF)"}
     else:

@@ -23,5 +23,7 @@ for _ in range(2):
     qet = q2.msed(E, S, 6.0, 3, 4, "posthoc", "cols")                    # MS(E^T)
     qxt = q2.msed(qx, S, 6.0, 5, 4, "posthoc", "tape")                   # MS(X^T) from the tape
     dw = q2.gemm(qet, qxt, torch.float32)                                # wgrad
+    qwt = q2.msed(qw, S, 6.0, 6, 2, "posthoc", "tape")                   # MS(W^T) from the tape
+    dx = q2.gemm(qe, qwt, torch.bfloat16)                                # dgrad
     torch.cuda.synchronize()
 q2.check_errors()
