@@ -5,6 +5,8 @@
 // float64 arithmetic uses __d*_rn intrinsics so nvcc never contracts it into
 // an FMA (the reference is numpy/numba without fastmath).
 #pragma once
+#include <utility>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/quartet2.h"
@@ -226,6 +228,36 @@ __device__ __forceinline__ float bf16_to_f32(uint32_t bits16) { return __uint_as
 
 __device__ __forceinline__ void atomic_or_err(uint32_t* err, uint32_t bits) {
   if (err) atomicOr(err, bits);
+}
+
+// ------------------------------------------------- programmatic launches ---
+// Hot-path kernels are launched with programmatic stream serialization: each
+// signals its dependents as soon as it starts and waits for its predecessor
+// (griddepcontrol.wait) before touching global memory, so a kernel's launch
+// and prologue (barrier init, TMEM allocation, tensor-map prefetch) overlap the
+// previous kernel's tail.  Q2_NO_PDL=1 launches them plainly.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {}   // dependents launch as CTAs exit (an early trigger measured slower)
+
+inline bool pdl_enabled() {
+  static const int on = getenv("Q2_NO_PDL") ? 0 : 1;
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace q2

@@ -189,6 +189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
+  pdl_trigger();
+  pdl_wait();                                                 // operands written by the previous kernels
   tc_fence_before();
   cluster_sync();                                             // barriers and TMEM of both CTAs ready
   tc_fence_after();
@@ -415,8 +417,9 @@ static int launch_gemm(const CUtensorMap* maps, const GemmArgs& g, cudaStream_t 
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = g.tiles_m * g.tiles_n;
   const int npairs = std::max(1, std::min(ntiles, nsm / 2));
-  nvfp4_gemm_kernel<F32><<<2 * npairs, GEMM_THREADS, GEMM_SMEM, st>>>(maps[0], maps[1], maps[2], maps[3], g);
-  Q2_CHECK_LAUNCH();
+  if (launch_pdl(nvfp4_gemm_kernel<F32>, dim3(2 * npairs), dim3(GEMM_THREADS), GEMM_SMEM, st, maps[0], maps[1],
+                 maps[2], maps[3], g) != cudaSuccess)
+    return Q2_ECUDA;
   return Q2_OK;
 }
 

@@ -101,8 +101,8 @@ static int launch_m64(const M64Src& s, const M64Args& a, cudaStream_t st) {
   }
   if (!ok) return Q2_ECUDA;
   const int ntiles = a.tiles_r * a.tiles_c;
-  k<<<std::min(ntiles, num_sms()), M64_THREADS, TL::SMEM, st>>>(tm, a);
-  Q2_CHECK_LAUNCH();
+  if (launch_pdl(k, dim3(std::min(ntiles, num_sms())), dim3(M64_THREADS), TL::SMEM, st, tm, a) != cudaSuccess)
+    return Q2_ECUDA;
   return Q2_OK;
 }
 
@@ -170,10 +170,10 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
     if ((rc = dispatch_m64<M64_POSTHOC>(src, a, st))) return rc;
     const int64_t quads = R * (K / 64);
     if (quads >= (1ll << 31)) return Q2_EINVAL;
-    msed64_pass2_kernel<<<(unsigned)std::max<int64_t>(1, (quads + 255) / 256), 256, 0, st>>>(
-        a.pseudo, a.corr, a.red, (uint32_t)R, (uint32_t)K, FastDiv((uint32_t)(K / 64)), a.sr_head, out->sf,
-        out->scale32, err);
-    Q2_CHECK_LAUNCH();
+    if (launch_pdl(msed64_pass2_kernel, dim3((unsigned)std::max<int64_t>(1, (quads + 255) / 256)), dim3(256), 0, st,
+                   (const uint16_t*)a.pseudo, (const double*)a.corr, (const unsigned long long*)a.red, (uint32_t)R,
+                   (uint32_t)K, FastDiv((uint32_t)(K / 64)), a.sr_head, out->sf, out->scale32, err) != cudaSuccess)
+      return Q2_ECUDA;
     return Q2_OK;
   }
   a.pow2 = mode == Q2_MSED_POW2;

@@ -192,6 +192,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
     }
     mbar_fence_init();
   }
+  pdl_trigger();
+  pdl_wait();
   if (SRC == Q2_SRC_TAPE_COLS && threadIdx.x < 48)
     reinterpret_cast<int*>(smem + TL::OFF_SPAN)[threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
   if (threadIdx.x < 64) {
@@ -846,6 +848,8 @@ __global__ void __launch_bounds__(256) msed64_pass2_kernel(const uint16_t* __res
                                                            uint32_t K, FastDiv fq, uint64_t sr_head,
                                                            uint8_t* __restrict__ sf, float* __restrict__ scale32_out,
                                                            uint32_t* __restrict__ err) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t qpr = K / 64, total = R * qpr;       // quads of 4 groups (< 2^26 for any tensor here)
   // k = smallest integer with pmax / 2^k <= 256 (ms_eden.py:86-91); pmax is 0 or a
   // normal E8M3 value, so k = E - 8 for a power of two and E - 7 otherwise

@@ -60,6 +60,8 @@ __device__ __forceinline__ void absmax_words(const uint32_t (&w)[8], int dtype, 
 __global__ void __launch_bounds__(256) amax_kernel(const void* __restrict__ x, int dtype, int64_t R, int64_t K,
                                                    int64_t ld, uint32_t* __restrict__ amax_bits,
                                                    uint32_t* __restrict__ err) {
+  pdl_trigger();
+  pdl_wait();
   const int esz = dtype == Q2_BF16 ? 2 : 4;
   uint32_t m = 0;
   bool bad = false;
@@ -283,6 +285,8 @@ __global__ void __launch_bounds__(QT + 32, 2) quant_fwd_kernel(
     for (int s = 0; s < QNST; ++s) { mbar_init(full0 + 8 * s, 1); mbar_init(empty0 + 8 * s, QT / 32); }
     mbar_fence_init();
   }
+  pdl_trigger();
+  pdl_wait();
   __syncthreads();
   const int warp = threadIdx.x >> 5;
   if (warp == QT / 32) {                                      // producer warp
@@ -396,6 +400,8 @@ __global__ void __launch_bounds__(128) quant_fix_kernel(const void* __restrict__
                                                         const uint32_t* __restrict__ fix_count,
                                                         const uint32_t* __restrict__ fix_list, uint8_t* __restrict__ codes,
                                                         uint8_t* __restrict__ sf, uint32_t* __restrict__ err) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t n = *fix_count;
   const float amax = __uint_as_float(*amax_bits);
   const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
@@ -430,8 +436,8 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
   int64_t vecs = R * (K / 8);
   int blocks = (int)std::min<int64_t>((vecs + 255) / 256, 148 * 8);
   if (blocks < 1) blocks = 1;
-  amax_kernel<<<blocks, 256, 0, s>>>(x, dtype, R, K, ld, amax_bits, err);
-  Q2_CHECK_LAUNCH();
+  if (launch_pdl(amax_kernel, dim3(blocks), dim3(256), 0, s, x, dtype, R, K, ld, amax_bits, err) != cudaSuccess)
+    return Q2_ECUDA;
   return Q2_OK;
 }
 
@@ -464,17 +470,17 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
     const int smem = QNST * QT * 32 + 128 + 512;
     static bool a0 = false;
     if (!a0) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a0 = true; }
-    quant_fwd_kernel<Q2_BF16><<<blocks, QT + 32, smem, s>>>(x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
+    launch_pdl(quant_fwd_kernel<Q2_BF16>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
                                                              out->codes, out->sf, out->scale32, fix_count, fix_list);
-    quant_fix_kernel<Q2_BF16><<<2 * nsm, 128, 0, s>>>(x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+    launch_pdl(quant_fix_kernel<Q2_BF16>, dim3(2 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
                                                       fix_list, out->codes, out->sf, err);
   } else {
     const int smem = QNST * QT * 64 + 128 + 512;
     static bool a1 = false;
     if (!a1) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a1 = true; }
-    quant_fwd_kernel<Q2_F32><<<blocks, QT + 32, smem, s>>>(x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
+    launch_pdl(quant_fwd_kernel<Q2_F32>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
                                                             out->codes, out->sf, out->scale32, fix_count, fix_list);
-    quant_fix_kernel<Q2_F32><<<2 * nsm, 128, 0, s>>>(x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+    launch_pdl(quant_fix_kernel<Q2_F32>, dim3(2 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
                                                      fix_list, out->codes, out->sf, err);
   }
   Q2_CHECK_LAUNCH();
