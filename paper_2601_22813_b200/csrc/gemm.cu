@@ -225,10 +225,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         if (tc >= 1) mbar_wait(bar_acce, (tc - 1) & 1);       // both epilogues drained the accumulator
         tc_fence_after();
         if (g.trace && pair == 0 && tc < 64) g.trace[4 * tc] = gtime();
+        unsigned long long wf = 0, ws = 0;
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
+          const unsigned long long t0 = g.trace ? gtime() : 0;
           mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
+          const unsigned long long t1 = g.trace ? gtime() : 0;
           mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
+          if (g.trace) { wf += t1 - t0; ws += gtime() - t1; }
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE);
           const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_ST);
@@ -242,7 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tc2_commit(bar_empty + 8 * s);
         }
         tc2_commit(bar_accf);
-        if (g.trace && pair == 0 && tc < 64) g.trace[4 * tc + 1] = gtime();
+        if (g.trace && pair == 0 && tc < 64) { g.trace[4 * tc + 1] = gtime(); g.trace[256 + 2 * tc] = wf; g.trace[257 + 2 * tc] = ws; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -251,11 +255,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // scale vector; lane L holds rows 32c + L (c = column within a 4-group).
     const int sp = warp - 4;
     const uint32_t trow = (uint32_t)(sp * 32) << 16;
-    int it = 0;
-    for (int t = pair; t < ntiles; t += npairs) {
+    int it = 0, tcs = 0;
+    const bool tr = g.trace && pair == 0 && rank == 0 && sp == 0;
+    for (int t = pair; t < ntiles; t += npairs, ++tcs) {
+      unsigned long long wsff = 0, wproc = 0;
       for (int kt = 0; kt < g.nk; ++kt, ++it) {
         const int s = it % STAGES;
+        const unsigned long long t0 = tr ? gtime() : 0;
         mbar_wait_sleep(bar_sff + 8 * s, (it / STAGES) & 1);
+        const unsigned long long t1 = tr ? gtime() : 0;
         const unsigned char* sfa = smem + s * STAGE + A_ST + B_ST;
         const unsigned char* sfb = sfa + SFA_ST;
         const uint32_t tsf = tmem + trow + SF_COL + SF_SLOT * s;
@@ -270,11 +278,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                        ::"r"(tsf + 12 * kk + 4), "r"(b0.x), "r"(b0.y), "r"(b0.z), "r"(b0.w), "r"(b1.x), "r"(b1.y),
                        "r"(b1.z), "r"(b1.w) : "memory");
         }
+        const unsigned long long t2 = tr ? gtime() : 0;
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(bar_sfr + 8 * s);
+        if (tr) { wsff += t2 - t1; wproc += gtime() - t2; }
       }
+      if (tr && lane == 0 && tcs < 64) { g.trace[384 + 2 * tcs] = wsff; g.trace[385 + 2 * tcs] = wproc; }
     }
   } else if (warp >= 8) {
     // ---------------- epilogue ----------------
@@ -441,18 +452,19 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
       !make_sf_map(&maps[2], a->sf, a->R, a->K, 1, 16) || !make_sf_map(&maps[3], b->sf, b->R, b->K, 2, 16))
     return Q2_ECUDA;
   static unsigned long long* trace = nullptr;
-  if (getenv("Q2_GEMM_TRACE") && !trace) cudaMalloc(&trace, 64 * 4 * 8);
+  if (getenv("Q2_GEMM_TRACE") && !trace) cudaMalloc(&trace, 64 * 8 * 8);
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
              (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_TRACE") ? trace : nullptr};
-  if (g.trace) cudaMemsetAsync(trace, 0, 64 * 4 * 8, static_cast<cudaStream_t>(stream));
+  if (g.trace) cudaMemsetAsync(trace, 0, 64 * 8 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int rc = d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
   if (g.trace) {
-    unsigned long long h[256];
+    unsigned long long h[512];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
     for (int i = 0; i < 12; ++i)
-      fprintf(stderr, "tile %d: mma %.2f us, accf->wake %.2f, wake->release %.2f, release->next start %.2f\n", i,
-              (h[4 * i + 1] - h[4 * i]) / 1e3, (h[4 * i + 2] - h[4 * i + 1]) / 1e3, (h[4 * i + 3] - h[4 * i + 2]) / 1e3,
+      fprintf(stderr, "tile %d: mma %.2f us (waits: operands %.2f, scales %.2f; scale warp: lds+st %.2f, wait::st+arrive %.2f), "
+              "accf->wake %.2f, wake->release %.2f, release->next start %.2f\n", i, (h[4 * i + 1] - h[4 * i]) / 1e3,
+              h[256 + 2 * i] / 1e3, h[257 + 2 * i] / 1e3, h[384 + 2 * i] / 1e3, h[385 + 2 * i] / 1e3, (h[4 * i + 2] - h[4 * i + 1]) / 1e3, (h[4 * i + 3] - h[4 * i + 2]) / 1e3,
               (h[4 * i + 4] - h[4 * i + 3]) / 1e3);
   }
   return rc;

@@ -1,10 +1,21 @@
-import os, sys, torch
-sys.path.insert(0, '/root/repo')
-import paper_2601_22813_b200 as q2
+"""Per-tile GEMM timeline (Q2_GEMM_TRACE=1): fprop, dgrad-like and wgrad-like shapes.
+
+    Q2_GEMM_TRACE=1 python tools/gemm_trace_probe.py
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2601_22813_b200 as q2  # noqa: E402
+
 g = torch.Generator(device="cuda").manual_seed(0)
-X = torch.randn(16384, 2048, device="cuda", generator=g).bfloat16()
-W = (torch.randn(11264, 2048, device="cuda", generator=g) / 45).bfloat16()
-qx, qw = q2.quantize_rtn_46(X), q2.quantize_rtn_46(W)
-for _ in range(3):
-    y = q2.gemm(qx, qw, torch.bfloat16)
-torch.cuda.synchronize()
+for name, (m, n, k) in (("fprop K=2048", (16384, 11264, 2048)), ("dgrad K=11264", (16384, 2048, 11264))):
+    A = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(n, k, device="cuda", generator=g) / 45).bfloat16()
+    qa, qb = q2.quantize_rtn_46(A), q2.quantize_rtn_46(B)
+    print(name, flush=True)
+    for _ in range(2):
+        y = q2.gemm(qa, qb, torch.bfloat16)
+    torch.cuda.synchronize()
