@@ -67,7 +67,9 @@ static int check_src(const M64Src& s, int64_t R, int64_t K) {
     if (reinterpret_cast<uintptr_t>(s.tape->codes) & 15) return Q2_EINVAL;
     return Q2_OK;
   }
-  if (!s.x || (s.dtype != Q2_BF16 && s.dtype != Q2_F32)) return Q2_EINVAL;
+  if (s.dtype != Q2_BF16 && s.dtype != Q2_F32) return Q2_EINVAL;
+  if (R == 0 || K == 0) return Q2_OK;                   // empty: nothing is read
+  if (!s.x) return Q2_EINVAL;
   const int esz = s.dtype == Q2_BF16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(s.x) & 15u) || (s.ld * esz) % 16) return Q2_EINVAL;
   if (s.kind == Q2_SRC_ROWS && s.ld < K) return Q2_EINVAL;

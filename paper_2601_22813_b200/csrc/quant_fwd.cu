@@ -449,6 +449,8 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
                      uint32_t* err, void* stream) {
   if (!out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (R == 0 || K == 0)                                   // empty tensor: the zero tensor (quantizers.py:219-220)
+    return cudaMemsetAsync(out->scale32, 0, 4, s) == cudaSuccess ? Q2_OK : Q2_ECUDA;
   uint32_t* amax_ws = static_cast<uint32_t*>(ws);
   uint32_t* fix_count = amax_ws + 1;
   uint32_t* fix_list = amax_ws + 4;

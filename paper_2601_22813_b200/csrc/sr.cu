@@ -205,14 +205,15 @@ extern "C" size_t q2_quant_sr_ws_bytes(void) { return 16; }
 extern "C" int q2_quant_sr(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0,
                            double cap1, double margin, double scale_div, uint64_t seed, uint64_t stream0,
                            uint64_t stream1, const q2_nvfp4* out, void* ws, uint32_t* err, void* stream) {
-  if (!x || !out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K || R < 0 || K % 16 || ld != K)
+  if (!out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K || R < 0 || K % 16 || ld != K)
     return Q2_EINVAL;
   if (dtype != Q2_BF16 && dtype != Q2_F32) return Q2_EINVAL;
-  if (reinterpret_cast<uintptr_t>(x) & 31u) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (R == 0 || K == 0)                                   // empty tensor: the zero tensor (quantizers.py:147-149)
+    return cudaMemsetAsync(out->scale32, 0, 4, s) == cudaSuccess ? Q2_OK : Q2_ECUDA;
+  if (!x || (reinterpret_cast<uintptr_t>(x) & 31u)) return Q2_EINVAL;
   uint32_t* amax = static_cast<uint32_t*>(ws);
   if (cudaMemsetAsync(amax, 0, 4, s) != cudaSuccess) return Q2_ECUDA;
-  if (R == 0) return cudaMemsetAsync(out->scale32, 0, 4, s) == cudaSuccess ? Q2_OK : Q2_ECUDA;
   int rc = q2_amax(x, dtype, R, K, ld, amax, err, stream);
   if (rc) return rc;
   const int64_t groups = R * (K / 16);

@@ -243,3 +243,12 @@ def test_quantize_rtn_46_producer_amax(cuda, family):
     a, b = q2.quantize_rtn_46(x), q2.quantize_rtn_46(x, amax=am)
     for u, v in zip(a.to_reference(), b.to_reference()):       # (sf padding rows are unspecified)
         assert np.array_equal(np.asarray(u), np.asarray(v))
+
+
+def test_empty_inputs(cuda):
+    """Zero-row tensors quantize to the zero tensor (quantizers.py:174-176, 219-220; ms_eden.py:135-137)."""
+    q2 = _q2()
+    e = torch.zeros(0, 256, device="cuda", dtype=torch.bfloat16)
+    for t in (q2.quantize_rtn_46(e), q2.quantize_rtn(e), q2.ms_eden_quantize(e, q2.SeedPair(1, 2)),
+              q2.posthoc_quantize(e, q2.SeedPair(1, 2)), q2.quantize_sr_46(e, 1, 2)):
+        assert t.shape == (0, 256) and float(t.scale32) == 0.0

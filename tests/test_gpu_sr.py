@@ -188,3 +188,23 @@ def test_identity_schemes_linear(cuda, cfg_args):
         got = got.double().cpu().numpy()
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-5, rel
+
+
+def test_baseline_quantizer_errors(cuda):
+    """The reference's input checks (quantizers.py:114-120, :276-280) on the baseline quantizers."""
+    import torch
+    q2 = _q2()
+    bad = np.ones((32, 64), np.float32)
+    bad[3, 5] = np.inf
+    for fn in (lambda v: q2.quantize_sr(v, 1, 2), lambda v: q2.quantize_sr_46(v, 1, 2),
+               lambda v: q2.quantize_square_block(v)):
+        with pytest.raises(ValueError, match="finite"):
+            fn(_dev(bad, False))
+    with pytest.raises(ValueError, match="multiple of 16"):
+        q2.quantize_sr(torch.ones(4, 24, device="cuda"), 1)
+    with pytest.raises(ValueError, match="2D with both dims multiples of 16"):
+        q2.quantize_square_block(torch.ones(24, 32, device="cuda"))
+    with pytest.raises(ValueError, match="multiple of 128"):
+        q2.rht_sr(torch.ones(32, 64, device="cuda"), q2.SeedPair(1, 2), 3, 4)
+    z = q2.quantize_sr(torch.zeros(0, 64, device="cuda"), 1, 2)
+    assert z.shape == (0, 64) and float(z.scale32) == 0.0
