@@ -30,3 +30,18 @@ def test_concentration_unbiased_vs_biased(cuda):
     assert -1.2 <= good.slope <= -0.8, good.to_dict()
     bad = H.concentration("four_over_six_backward", b_max=256, trials=1, seed=3)
     assert bad.tail_slope > -0.6, bad.to_dict()
+
+
+def test_grad_check_identity(cuda):
+    from paper_2601_22813_b200 import harness as H
+    r = H.grad_check("identity", seed=0, n_probes=16)
+    assert r.max_rel_err < 1e-3, r.to_dict()          # float64 central differences of a ~1e4 loss
+
+
+def test_train_demo_quartet2_learns(cuda):
+    """QAT demo (harness.py:375-458) on the B200 layers: quartet2 tracks the unquantized run."""
+    from paper_2601_22813_b200 import harness as H
+    runs = H.train_demo(("identity", "quartet2"), steps=300, n_seeds=1)
+    ident, q = runs
+    assert q.losses[-1] < 0.5 * q.losses[0], q.losses[[0, -1]]
+    assert q.final_loss < 3.0 * ident.final_loss, (q.final_loss, ident.final_loss)
