@@ -52,7 +52,10 @@ constexpr int GEMM_SMEM = OFF_BAR + 256 + 1024;
 constexpr int GEMM_THREADS = 512;
 constexpr int TMEM_COLS = 512;
 constexpr int SF_COL = 256, SF_SLOT = 48;                 // per stage: 4 x (SFA 4 + SFB 8) columns
-constexpr int GROUP_M = 8;
+#ifndef Q2_GROUP_M
+#define Q2_GROUP_M 8
+#endif
+constexpr int GROUP_M = Q2_GROUP_M;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;               // shared::cluster address of the leader's copy
 
 // instruction descriptor, kind::mxf4nvf4 (cute InstrDescriptorBlockScaled): a/b E2M1 (=1)
