@@ -30,8 +30,11 @@
 // ldmatrix.m8n8 delivers (.trans for E^T / tape sources).  Butterfly bits
 // 0 and 3..6 are lane-local, bits 1..2 cross lanes (shuffles).
 //
-// Persistent CTA: warp 8 is the TMA producer (STAGES-deep ring of 64-row x
-// 128-column tiles), warps 0..7 compute.
+// Persistent CTA of 16 compute warps (128-row x 128-column tiles, 8 rows per
+// warp) at 128 registers; thread 0 also keeps a STAGES-deep TMA ring full (a
+// non-blocking pump, refills retried until the slowest warp has released a
+// stage).  The tape source decodes each NVFP4 tile to f16 in shared memory
+// first (all 512 threads, then a CTA barrier).
 
 namespace q2 {
 
