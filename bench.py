@@ -185,6 +185,7 @@ def main():
 
     def step(i, instrument=False):
         seeds = q2.SeedPair(q2.derive_stream(1, i, rank), q2.derive_stream(2, i, rank))
+        pending = []                                      # dW all-reduces overlap the next projection
         for X, W, E in data:
             if instrument:
                 mark("fwd")
@@ -195,7 +196,9 @@ def main():
             if instrument:
                 mark("end")
             if world > 1:
-                dist.all_reduce(grads.dW)
+                pending.append(dist.all_reduce(grads.dW, async_op=True))
+        for h in pending:
+            h.wait()
         return y
 
     for i in range(args.warmup):
@@ -432,7 +435,7 @@ def e2e_measure(q2, data, cfg, args, world, dev):
             y, tape = q2.forward(X, W, cfg, out_dtype=torch.bfloat16)
             g = q2.backward(tape, E, seeds, dx_dtype=torch.bfloat16)
             if world > 1:
-                torch.distributed.all_reduce(g.dW)
+                torch.distributed.all_reduce(g.dW, async_op=True).wait()   # ordered before the D2H copy
             ev = torch.cuda.Event()
             ev.record(main)
             used[j] = ev
