@@ -68,13 +68,14 @@ template <int SRC, int DT>
 struct M64Tile {
   static constexpr int RAW = SRC == Q2_SRC_TAPE_COLS ? 8192 + 2048 : (DT == Q2_BF16 ? 32768 : 65536);
   static constexpr int STAGES = SRC == Q2_SRC_TAPE_COLS ? 6 : (DT == Q2_BF16 ? 4 : 3);
-  static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? 2 * 32768 : 0;     // decoded f16 tiles
+  static constexpr int NDEC = 3;                                          // decoded tiles in flight (tape)
+  static constexpr int DEC = SRC == Q2_SRC_TAPE_COLS ? NDEC * 32768 : 0;  // decoded f16 tiles
   static constexpr int OFF_DEC = STAGES * RAW;
   static constexpr int OFF_CST = OFF_DEC + DEC;                           // code staging, 16 x 640 B
   static constexpr int OFF_SGN = OFF_CST + M64_WARPS * 640;              // 4 x 16 sign words
-  static constexpr int OFF_SPAN = OFF_SGN + 256;                          // tape: 3 x 8 groups x (min, max)
-  static constexpr int OFF_BAR = OFF_SPAN + 3 * 8 * 8;
-  static constexpr int SMEM = OFF_BAR + 128 + 1024;
+  static constexpr int OFF_SPAN = OFF_SGN + 256;                          // tape: NDEC x 16 warps x 2 x (min, max)
+  static constexpr int OFF_BAR = OFF_SPAN + NDEC * 16 * 4 * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -186,6 +187,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(m64_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TL::OFF_BAR);
   const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + TL::STAGES);
+  // tape: decoded tile b complete (every warp decoded its part) / consumed (every warp loaded it)
+  const uint32_t bar_dfull = smem_u32(bars + 2 * TL::STAGES), bar_dempty = smem_u32(bars + 2 * TL::STAGES + TL::NDEC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.tiles_r * a.tiles_c;
   if (threadIdx.x == 0) {
@@ -193,12 +196,15 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, M64_WARPS);
     }
+    if (SRC == Q2_SRC_TAPE_COLS)
+      for (int b = 0; b < TL::NDEC; ++b) {
+        mbar_init(bar_dfull + 8 * b, M64_WARPS);
+        mbar_init(bar_dempty + 8 * b, M64_WARPS);
+      }
     mbar_fence_init();
   }
   pdl_trigger();
   pdl_wait();
-  if (SRC == Q2_SRC_TAPE_COLS && threadIdx.x < 48)
-    reinterpret_cast<int*>(smem + TL::OFF_SPAN)[threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
   if (threadIdx.x < 64) {
     const int qq = threadIdx.x >> 4, k = threadIdx.x & 15, e = 8 * k + 2 * qq;
     const uint32_t s0 = (a.sign[e >> 5] >> (e & 31)) & 1u, s1 = (a.sign[(e + 1) >> 5] >> ((e + 1) & 31)) & 1u;
@@ -294,37 +300,31 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
   uint64_t wabs = 0, wp = 0;                          // running |y| max / pseudo max (f64 bits)
   bool bad = false, ovf = false, nanscale = false;
 
-  int it = 0;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int tr = (int)a.fc.div((uint32_t)t), tc = t - tr * a.tiles_c;
-    const int s = it % TL::STAGES;
-    if (threadIdx.x == 0) pump(it, true);
-    mbar_wait_sleep(bar_full + 8 * s, (it / TL::STAGES) & 1);
-    const uint32_t st = smem_u32(smem + s * TL::RAW);
-    const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
-    double y[16][2];
-    bool fwht_done = false;
-
-    if (SRC == Q2_SRC_TAPE_COLS) {
+  // Tape source: decode tile j of this CTA (its NVFP4 codes and scales, raw ring
+  // stage j % STAGES) into f16 buffer j % NDEC, one tile ahead of the compute,
+  // so no CTA-wide barrier sits between decoding and transforming a tile.
+  auto decode_tile = [&](int j) {
+    const int tj = blockIdx.x + j * gridDim.x;
+    const int trj = (int)a.fc.div((uint32_t)tj), tcj = tj - trj * a.tiles_c;
+    (void)trj;
+    const int sj = j % TL::STAGES, b = j % TL::NDEC;
+    if (j >= TL::NDEC) mbar_wait_sleep(bar_dempty + 8 * b, ((j / TL::NDEC) - 1) & 1);   // tile j - NDEC consumed
+    mbar_wait_sleep(bar_full + 8 * sj, (j / TL::STAGES) & 1);
       // decode the NVFP4 tape block [128 tape rows x 128 tape cols] into f16 (exact:
       // FP4*E4M3 has <= 6 significant bits), random sign of the tape row applied.
       // dec: two 64-column halves of [128 rows x 128 B], 16-B segments XOR-swizzled.
-      unsigned char* dec = smem + TL::OFF_DEC + (it & 1) * 32768;
+      unsigned char* dec = smem + TL::OFF_DEC + b * 32768;
       {
         const int tri = threadIdx.x & 127, h = threadIdx.x >> 7;               // tape row, 32-column quarter
-        const uint4 cw = *reinterpret_cast<const uint4*>(smem + s * TL::RAW + tri * 64 + h * 16);
+        const uint4 cw = *reinterpret_cast<const uint4*>(smem + sj * TL::RAW + tri * 64 + h * 16);
         const int L = tri & 31;
-        const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + s * TL::RAW + 8192 + (h >> 1) * 1024 +
-                                                                ((L >> 3) << 8) + ((tc & 1) << 7) + ((L & 7) << 4) +
+        const uint32_t sfw = *reinterpret_cast<const uint32_t*>(smem + sj * TL::RAW + 8192 + (h >> 1) * 1024 +
+                                                                ((L >> 3) << 8) + ((tcj & 1) << 7) + ((L & 7) << 4) +
                                                                 ((tri >> 5) << 2));
         const uint32_t neg = ((a.sign[tri >> 5] >> (tri & 31)) & 1u) ? 0x80008000u : 0u;
         uint32_t sc[2];
-        // per-group binade range of the tile's scales, triple-buffered: buffer
-        // (it+1)%3 was last read in iteration it-2, which every warp finished
-        // before the previous tile's barrier
-        int* span = reinterpret_cast<int*>(smem + TL::OFF_SPAN) + 16 * (it % 3);
-        if (threadIdx.x < 16)
-          reinterpret_cast<int*>(smem + TL::OFF_SPAN)[16 * ((it + 1) % 3) + threadIdx.x] = (threadIdx.x & 1) ? -64 : 64;
+        // per-group binade range of the tile's scales: this warp's (min, max) per group
+        int* spw = reinterpret_cast<int*>(smem + TL::OFF_SPAN) + (b * 16 + warp) * 4;
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           const uint32_t s8 = (sfw >> (8 * (2 * (h & 1) + g))) & 0xFF;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
             emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
             emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
           }
-          if (lane == 0) { atomicMin(&span[2 * (2 * h + g)], emin); atomicMax(&span[2 * (2 * h + g) + 1], emax); }
+          if (lane == 0) { spw[2 * g] = emin; spw[2 * g + 1] = emax; }
         }
         const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
         uint32_t o[16];
@@ -355,16 +355,50 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
               make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_empty + 8 * s);
-      named_bar(1, M64_THREADS);
+      if (lane == 0) {
+        mbar_arrive(bar_empty + 8 * sj);                      // raw stage free
+        mbar_arrive(bar_dfull + 8 * b);                       // this warp's part of tile j decoded
+      }
+  };
+  if (SRC == Q2_SRC_TAPE_COLS && nmine > 0) decode_tile(0);
+
+  int it = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int tr = (int)a.fc.div((uint32_t)t), tc = t - tr * a.tiles_c;
+    const int s = it % TL::STAGES;
+    if (threadIdx.x == 0) pump(it, true);
+    if (SRC != Q2_SRC_TAPE_COLS) mbar_wait_sleep(bar_full + 8 * s, (it / TL::STAGES) & 1);
+    const uint32_t st = smem_u32(smem + s * TL::RAW);
+    const int64_t r = (int64_t)tr * M64_ROWS + 8 * warp + rw;   // logical row of this lane
+    double y[16][2];
+    bool fwht_done = false;
+
+    if (SRC == Q2_SRC_TAPE_COLS) {
+      // tile it was decoded (into buffer it % NDEC) one iteration ahead; decode tile it+1 now
+      if (it + 1 < nmine) {
+        if (threadIdx.x == 0) pump(it + 1, true);
+        decode_tile(it + 1);
+      }
+      const int db_i = it % TL::NDEC;
+      mbar_wait_sleep(bar_dfull + 8 * db_i, (it / TL::NDEC) & 1);
+      unsigned char* dec = smem + TL::OFF_DEC + db_i * 32768;
       const uint32_t db = smem_u32(dec);
       // Exact fp32 route: FP4*E4M3 values have <= 6 significant bits, so when the
       // tile's scales for this warp's group span <= 7 binades every partial sum of
       // the 128-point transform fits 24 bits: the fp32 FWHT of the unscaled values
       // is exact, and fl64(fl64(sum * scale32) * c) is the reference's
       // fl64(FWHT(x * scale32) * c) (all of its float64 partial sums are exact too).
-      const int* sp = reinterpret_cast<const int*>(smem + TL::OFF_SPAN) + 16 * (it % 3) + 2 * (warp >> 1);
-      fwht_done = sp[1] - sp[0] <= 7;                          // warp-uniform (one group per warp)
+      {
+        const int* spw = reinterpret_cast<const int*>(smem + TL::OFF_SPAN) + db_i * 64;
+        const int hq = warp >> 2, gq = (warp >> 1) & 1;        // this warp's group 2*hq + gq, decoded by warps 4hq..4hq+3
+        int emin = 64, emax = -64;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          emin = min(emin, spw[(4 * hq + w) * 4 + 2 * gq]);
+          emax = max(emax, spw[(4 * hq + w) * 4 + 2 * gq + 1]);
+        }
+        fwht_done = emax - emin <= 7;                          // warp-uniform (one group per warp)
+      }
       if (!rot) fwht_done = false;                             // unrotated: y = dequantized value
       float z[16][2];
 #pragma unroll
@@ -377,6 +411,8 @@ __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_con
           asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
               : "=f"(z[4 * i + j][0]), "=f"(z[4 * i + j][1]) : "r"(v[j]));
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_dempty + 8 * db_i);       // decoded buffer may be refilled
       if (fwht_done) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
