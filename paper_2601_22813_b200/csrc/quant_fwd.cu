@@ -263,6 +263,160 @@ __device__ __forceinline__ float s_bound(float S, float Q) {
   return 0x1p-17f * 1.01f * sqrtf(S * Q) + 0x1p-35f * Q + 0x1p-20f * S;
 }
 
+// ----- fix-up pass: the same certified decision with exact tie/midpoint resolution -----
+template <bool TIES>
+__device__ __forceinline__ BranchConst branch_const_t(float gmax, float invD, float capf, float s32f, const float* mids) {
+  BranchConst c;
+  const float y = gmax * invD;
+  c.s8 = cvt_e4m3_rn(y);
+  const float mlo = c.s8 > 0 ? mids[c.s8 - 1] : -1.f, mhi = mids[c.s8];   // mids[126] = +inf
+  const bool nlo = !(y > mlo * (1.0f + 0x1p-20f)), nhi = !(y < mhi * (1.0f - 0x1p-20f));
+  c.bad = nlo | nhi;
+  if (TIES && c.bad) {
+    const uint32_t j = nlo ? c.s8 - 1u : c.s8;
+    const float P = mids[j] * capf;
+    const float th = __fmul_rn(P, s32f), tl = __fmaf_rn(P, s32f, -th);
+    const float diff = __fsub_rn(gmax, th);
+    c.bad = __fmaf_rn(mids[j], capf, -P) != 0.f || !(th >= 0x1p-100f) || j > 125u;
+    c.s8 = (diff > tl || (diff == tl && (j & 1u))) ? j + 1u : j;
+  }
+  c.E = e4m3_valf(c.s8);
+  const float d32 = c.E * s32f;                     // relative error <= 2^-24 vs E*scale32
+  c.bad |= !(d32 >= 0x1p-125f);
+  float inv;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d32));
+  c.inv = inv;
+  const float lo = inv * (1.0f - 0x1p-19f), hi = inv * (1.0f + 0x1p-19f);
+  c.ilo = pack2(lo, lo);
+  c.ihi = pack2(hi, hi);
+  return c;
+}
+
+__device__ __forceinline__ float fp4_magf(uint32_t m) {
+  return m < 5u ? 0.5f * (float)m : (m == 5u ? 3.f : (m == 6u ? 4.f : 6.f));
+}
+
+// One branch over the 16 elements: codes, certification, S = sum (rho - q)^2.
+// Elements whose two quotient brackets straddle an E2M1 rounding threshold t
+// are uncertain; TIES decides them exactly in fp32 -- |v| vs t*d with
+// d = E*scale32 as th + tl (t*E exact, FMA residual), |v| - th exact by
+// Sterbenz, a tie takes the even code (_nb_rtn's rint) -- and corrects S by the
+// changed residual.  elem(k) re-reads element k.
+template <bool TIES, class Elem>
+__device__ __forceinline__ void run_branch_t(const uint64_t (&vv)[8], const BranchConst& c, float s32f, Elem elem,
+                                           uint32_t& lo, uint32_t& hi, bool& unc, float& S) {
+  uint32_t l2, h2;
+  float e[8];
+  uint64_t acc = 0;
+  const uint64_t (&va)[4] = *reinterpret_cast<const uint64_t(*)[4]>(&vv[0]);
+  const uint64_t (&vb)[4] = *reinterpret_cast<const uint64_t(*)[4]>(&vv[4]);
+  branch8(va, c.ilo, c.ihi, lo, l2, e);
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) ffma2_acc(acc, e[k], e[k + 1]);
+  branch8(vb, c.ilo, c.ihi, hi, h2, e);
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) ffma2_acc(acc, e[k], e[k + 1]);
+  S = hsum2(acc);
+  if (!TIES) {
+    unc |= (lo != l2) | (hi != h2);
+  } else if (((lo != l2) | (hi != h2)) && !c.bad) {
+    const float ilo = __uint_as_float((uint32_t)c.ilo);
+    uint64_t w = (uint64_t)lo | ((uint64_t)hi << 32);
+    uint64_t dd = (uint64_t)(lo ^ l2) | ((uint64_t)(hi ^ h2) << 32);
+    while (dd) {
+      const int k = (__ffsll((long long)dd) - 1) >> 2;
+      dd &= ~(0xFull << (4 * k));
+      const float v = elem(k);
+      const uint32_t m = (uint32_t)(w >> (4 * k)) & 7u;
+      const float t = 0.5f * (fp4_magf(m) + fp4_magf(m + 1));
+      const float p = t * c.E;                                    // <= 7 significant bits: exact
+      const float th = __fmul_rn(p, s32f), tl = __fmaf_rn(p, s32f, -th);
+      const float diff = __fsub_rn(fabsf(v), th);
+      if (diff > tl || (diff == tl && (m & 1u))) {
+        const float rho = __fmul_rz(v, ilo), sg = v < 0.f ? -1.f : 1.f;
+        const float eo = sg * fp4_magf(m) - rho, en = sg * fp4_magf(m + 1) - rho;
+        S += en * en - eo * eo;
+        w += 1ull << (4 * k);
+      }
+    }
+    lo = (uint32_t)w;
+    hi = (uint32_t)(w >> 32);
+  }
+}
+
+struct QuantConst {
+  float invD0, invD1, cap0f, cap1f, s32f;
+  int ncaps;
+};
+
+// Certified fp32 decision for one 16-group (vv: 8 packed element pairs, gmax > 0):
+// codes, scale and the 4/6 choice; false when the group needs the float64
+// restatement.
+template <bool TIES, class Elem>
+__device__ __forceinline__ bool group_certified(const uint64_t (&vv)[8], float gmax, const QuantConst& q,
+                                                const float* mids, Elem elem, uint32_t& lo, uint32_t& hi, uint32_t& s8) {
+  uint64_t vacc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(vacc) : "l"(vv[k]));
+  const float V = hsum2(vacc);
+  const BranchConst c0 = branch_const_t<TIES>(gmax, q.invD0, q.cap0f, q.s32f, mids);
+  bool unc = c0.bad;
+  float S0;
+  uint32_t lo0, hi0;
+  run_branch_t<TIES>(vv, c0, q.s32f, elem, lo0, hi0, unc, S0);
+  if (q.ncaps == 1) {
+    lo = lo0; hi = hi0; s8 = c0.s8;
+    return !unc;
+  }
+  const BranchConst c1 = branch_const_t<TIES>(gmax, q.invD1, q.cap1f, q.s32f, mids);
+  unc |= c1.bad;
+  float S1;
+  uint32_t lo1, hi1;
+  run_branch_t<TIES>(vv, c1, q.s32f, elem, lo1, hi1, unc, S1);
+  const float Q0 = V * c0.inv * c0.inv * 1.001f, Q1 = V * c1.inv * c1.inv * 1.001f;
+  const float E0 = c0.E * c0.E, E1 = c1.E * c1.E;
+  const float A0 = E0 * S0, A1 = E1 * S1;
+  const float M = E0 * s_bound(S0, Q0) + E1 * s_bound(S1, Q1) + 0x1p-22f * (A0 + A1);
+  const bool pick1 = A1 + M < A0, pick0 = A0 + M < A1;      // strict: ties keep caps[0]
+  lo = pick1 ? lo1 : lo0; hi = pick1 ? hi1 : hi0; s8 = pick1 ? c1.s8 : c0.s8;
+  return !unc && (pick0 || pick1);
+}
+
+// Group words -> 8 packed f32 pairs and the group |x| max.
+template <int DT>
+__device__ __forceinline__ float unpack_group(const uint32_t (&w)[16], uint64_t (&vv)[8]) {
+  uint32_t m = 0;
+  if (DT == Q2_BF16) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t t = w[k] & 0x7FFF7FFFu;
+      asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(t));
+      vv[k] = pack2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
+    }
+    return __uint_as_float(max(m & 0xFFFFu, m >> 16) << 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    m = max(m, max(w[2 * k] & 0x7FFFFFFFu, w[2 * k + 1] & 0x7FFFFFFFu));
+    vv[k] = pack2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1]));
+  }
+  return __uint_as_float(m);
+}
+
+__device__ __forceinline__ QuantConst quant_const(float scale32, int ncaps, double cap0, double cap1, bool& fast_ok) {
+  QuantConst q;
+  const double s32 = (double)scale32;
+  q.invD0 = (float)(1.0 / __dmul_rn(s32, cap0));
+  q.invD1 = (float)(1.0 / __dmul_rn(s32, cap1));
+  q.cap0f = (float)cap0;
+  q.cap1f = (float)cap1;
+  q.s32f = scale32;
+  q.ncaps = ncaps;
+  // every d and 1/d stays normal in fp32; caps fp32-exact for the midpoint test
+  fast_ok = scale32 >= 0x1p-100f && (double)q.cap0f == cap0 && (double)q.cap1f == cap1;
+  return q;
+}
+
 // Persistent quantizer: a producer warp streams units of QT contiguous
 // 16-groups into a QNST-deep shared-memory ring with cp.async.bulk (TMA
 // engine); QT consumer threads quantize one group each per unit.  Fast path:
@@ -402,16 +556,44 @@ __global__ void __launch_bounds__(128) quant_fix_kernel(const void* __restrict__
                                                         uint8_t* __restrict__ sf, uint32_t* __restrict__ err) {
   pdl_trigger();
   pdl_wait();
+  __shared__ float mids[128];
+  for (int t = threadIdx.x; t < 127; t += blockDim.x)
+    mids[t] = t < 126 ? 0.5f * (e4m3_valf(t) + e4m3_valf(t + 1)) : __int_as_float(0x7f800000);
+  __syncthreads();
   const uint32_t n = *fix_count;
   const float amax = __uint_as_float(*amax_bits);
   const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
+  bool fast_ok;
+  const QuantConst qc = quant_const(scale32, ncaps, cap0, cap1, fast_ok);
   const int64_t gpr = K / GROUP, kpr = sf_kblocks(K);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t gid = fix_list[i];
     const uint32_t r = fgpr.div(gid), j = gid - r * (uint32_t)gpr;
-    const uint3 e = quant_group_exact<DT>(x, (int64_t)gid * GROUP, scale32, ncaps, cap0, cap1, err);
-    *reinterpret_cast<uint2*>(codes + (int64_t)gid * 8) = make_uint2(e.x, e.y);
-    sf_store(sf, r, j, kpr, (uint8_t)e.z);
+    uint32_t lo = 0, hi = 0, s8 = 0;
+    bool ok = false;
+    if (fast_ok) {
+      // most fix-ups are exact E2M1 ties or E4M3 midpoints: the fp32 path resolves them exactly
+      uint32_t w[16];
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(x) + (int64_t)gid * GROUP * (DT == Q2_BF16 ? 2 : 4));
+#pragma unroll
+      for (int q = 0; q < (DT == Q2_BF16 ? 2 : 4); ++q) {
+        const uint4 t = __ldg(src + q);
+        w[4 * q] = t.x; w[4 * q + 1] = t.y; w[4 * q + 2] = t.z; w[4 * q + 3] = t.w;
+      }
+      uint64_t vv[8];
+      const float gmax = unpack_group<DT>(w, vv);
+      auto elem = [&](int k) {
+        return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + (int64_t)gid * GROUP + k))
+                             : __ldg(static_cast<const float*>(x) + (int64_t)gid * GROUP + k);
+      };
+      ok = gmax > 0.f && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8);
+    }
+    if (!ok) {                                                // the literal float64 restatement
+      const uint3 e = quant_group_exact<DT>(x, (int64_t)gid * GROUP, scale32, ncaps, cap0, cap1, err);
+      lo = e.x; hi = e.y; s8 = e.z;
+    }
+    *reinterpret_cast<uint2*>(codes + (int64_t)gid * 8) = make_uint2(lo, hi);
+    sf_store(sf, r, j, kpr, (uint8_t)s8);
   }
 }
 
@@ -474,7 +656,7 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
     if (!a0) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a0 = true; }
     launch_pdl(quant_fwd_kernel<Q2_BF16>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
                                                              out->codes, out->sf, out->scale32, fix_count, fix_list);
-    launch_pdl(quant_fix_kernel<Q2_BF16>, dim3(2 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+    launch_pdl(quant_fix_kernel<Q2_BF16>, dim3(8 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
                                                       fix_list, out->codes, out->sf, err);
   } else {
     const int smem = QNST * QT * 64 + 128 + 512;
@@ -482,7 +664,7 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
     if (!a1) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a1 = true; }
     launch_pdl(quant_fwd_kernel<Q2_F32>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
                                                             out->codes, out->sf, out->scale32, fix_count, fix_list);
-    launch_pdl(quant_fix_kernel<Q2_F32>, dim3(2 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
+    launch_pdl(quant_fix_kernel<Q2_F32>, dim3(8 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
                                                      fix_list, out->codes, out->sf, err);
   }
   Q2_CHECK_LAUNCH();
