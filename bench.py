@@ -204,6 +204,10 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    # per-phase split from one instrumented eager step (before capture: the
+    # first eager step after a capture pays the allocator's cudaMallocs)
+    step(args.warmup, instrument=True)
+    torch.cuda.synchronize()
 
     # The step is captured once into a CUDA graph (kernels, memsets and the dW
     # all-reduce; host-side Python/ctypes launch overhead removed).  Seeds are
@@ -237,10 +241,6 @@ def main():
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end) / args.steps
-    # per-phase split from one instrumented eager step
-    events.clear()
-    step(args.warmup + args.steps, instrument=True)
-    torch.cuda.synchronize()
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
