@@ -14,6 +14,7 @@ from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_
 from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr, sr_operand
 from .linear_graph import (GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config, forward,
                            gemm, gemm_emulated)
+from .module import Quartet2Linear, Quartet2LinearFunction, quartet2_linear
 
 __all__ = [
     "CHUNK", "GROUP", "GUARDED_SCALE_CAP", "FP8_RTN_MARGIN", "SeedPair", "derive_stream", "prng_uniform",
@@ -22,4 +23,5 @@ __all__ = [
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
     "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
+    "Quartet2Linear", "Quartet2LinearFunction", "quartet2_linear",
 ]

@@ -11,6 +11,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from functools import lru_cache
 
+import numpy as np
+
 CHUNK = 128
 _M64 = (1 << 64) - 1
 _GOLDEN = 0x9E3779B97F4A7C15
@@ -64,13 +66,19 @@ def prng_uniform(seed: int, stream: int, index: int) -> float:
 
 @lru_cache(maxsize=1024)
 def sign_mask(seed: int, rotation_id: int) -> tuple:
-    """The rotation's 128 signs (rht.py:99-106) as four u32 words, bit i = sign i is -1."""
+    """The rotation's 128 signs (rht.py:99-106) as four u32 words, bit i = sign i is -1.
+
+    ``u < 0.5`` is ``(bits >> 11) * 2**-53 < 0.5``, i.e. bit 63 of ``_bits`` is
+    clear; the seed/stream prefix of ``_bits`` is shared, so the 128 index mixes
+    run as one uint64 vector (wrap-around arithmetic, same integers)."""
     stream = derive_stream(DOMAIN_SIGNS, rotation_id)
-    words = [0, 0, 0, 0]
-    for i in range(CHUNK):
-        if not prng_uniform(seed, stream, i) < 0.5:
-            words[i >> 5] |= 1 << (i & 31)
-    return tuple(words)
+    z0 = _mix64(_mix64((seed + _GOLDEN) & _M64) ^ ((stream + _GOLDEN) & _M64))
+    z = np.uint64(z0) ^ (np.arange(CHUNK, dtype=np.uint64) + np.uint64(_GOLDEN))
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    neg = ((z ^ (z >> np.uint64(31))) >> np.uint64(63)).astype(np.uint64)
+    words = (neg.reshape(4, 32) << np.arange(32, dtype=np.uint64)).sum(axis=1)
+    return tuple(int(w) for w in words)
 
 
 def sr_stream(tensor_id: int) -> int:

@@ -94,3 +94,13 @@ def test_constants_match_reference_arithmetic():
     assert (6.0 * q2.GUARDED_SCALE_CAP).hex() == "0x1.3c3c3c3c3c3c4p+11"
     from paper_2601_22813_b200.rht import INV_SQRT_CHUNK
     assert INV_SQRT_CHUNK.hex() == "0x1.6a09e667f3bcdp-4"
+
+
+def test_module_host_side():
+    import torch
+    import paper_2601_22813_b200 as q2
+    m = q2.Quartet2Linear(256, 128, bias=True, seed=5)
+    assert m.weight.shape == (128, 256) and m.weight.dtype == torch.bfloat16 and m.bias.shape == (128,)
+    assert m.seeds_for(3) == q2.SeedPair(q2.derive_stream(5, 1, 3), q2.derive_stream(5, 2, 3))
+    assert m.seeds_for(0) != q2.Quartet2Linear(256, 128, seed=6).seeds_for(0)
+    assert "posthoc=True" in repr(m)
