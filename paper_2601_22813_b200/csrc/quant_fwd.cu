@@ -422,10 +422,13 @@ __device__ __forceinline__ QuantConst quant_const(float scale32, int ncaps, doub
 // engine); QT consumer threads quantize one group each per unit.  Fast path:
 // certified fp32 decisions (interval-checked E2M1 codes, bounded 4/6 error
 // comparison); uncertain groups run quant_group_exact.
+#ifndef Q2_QMINB
+#define Q2_QMINB 2
+#endif
 constexpr int QT = 256, QNST = 4;
 
 template <int DT>
-__global__ void __launch_bounds__(QT + 32, 2) quant_fwd_kernel(
+__global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
     const void* __restrict__ x, int64_t R, int64_t K, int ncaps, double cap0, double cap1, double scale_div,
     FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
     float* __restrict__ scale32_out, uint32_t* __restrict__ fix_count, uint32_t* __restrict__ fix_list) {
@@ -616,7 +619,8 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
   if ((reinterpret_cast<uintptr_t>(x) & 31u) || (ld * esz) % 32) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int64_t vecs = R * (K / 8);
-  int blocks = (int)std::min<int64_t>((vecs + 255) / 256, 148 * 8);
+  static int bps = getenv("Q2_AMAX_BPS") ? atoi(getenv("Q2_AMAX_BPS")) : 4;   // 4 blocks/SM: one wave (tools/quant_probe.py sweep)
+  int blocks = (int)std::min<int64_t>((vecs + 255) / 256, 148 * bps);
   if (blocks < 1) blocks = 1;
   if (launch_pdl(amax_kernel, dim3(blocks), dim3(256), 0, s, x, dtype, R, K, ld, amax_bits, err) != cudaSuccess)
     return Q2_ECUDA;
@@ -648,7 +652,7 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, 2 * nsm));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, Q2_QMINB * nsm));
   const FastDiv fg((uint32_t)(K / 16));
   if (dtype == Q2_BF16) {
     const int smem = QNST * QT * 32 + 128 + 512;
