@@ -12,8 +12,8 @@ from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_
                       pass1, pass2,
                       posthoc_quantize)
 from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr, sr_operand
-from .linear_graph import (GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config, forward,
-                           gemm, gemm_emulated)
+from .linear_graph import (ABLATIONS, GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config,
+                           format_config, forward, gemm, gemm_emulated, parse_config)
 from .module import Quartet2Linear, Quartet2LinearFunction, quartet2_linear
 
 __all__ = [
@@ -23,5 +23,5 @@ __all__ = [
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
     "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
-    "Quartet2Linear", "Quartet2LinearFunction", "quartet2_linear",
+    "Quartet2Linear", "Quartet2LinearFunction", "quartet2_linear", "ABLATIONS", "format_config", "parse_config",
 ]

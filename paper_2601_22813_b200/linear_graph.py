@@ -26,6 +26,11 @@ from .sr import SquareBlockTensor, quantize_sr, quantize_sr_46, quantize_square_
 
 FORWARD_SCHEMES = ("rtn_1x16_46", "rtn_1x16", "rtn_16x16", "rtn_16x16_46", "identity")
 BACKWARD_SCHEMES = ("ms_eden", "sr_rht", "sr", "sr_46", "sr_rht_46", "identity")
+ABLATIONS = ("a", "b", "c", "d", "e", "full")
+# Operands each ablation quantizes: (E in dX, W^T in dX, E^T in dW, X^T in dW), linear_graph.py:59-70
+ABLATION_MASK = {"a": (False, False, True, True), "b": (True, False, False, False),
+                 "c": (True, True, False, False), "d": (True, False, True, True),
+                 "e": (True, True, True, True), "full": (True, True, True, True)}
 PAIR_DX = derive_stream(1)   # linear_graph.py:300
 PAIR_DW = derive_stream(2)   # linear_graph.py:301
 
@@ -55,9 +60,8 @@ def _keep(main: torch.cuda.Stream, *tensors) -> None:
 
 @dataclass(frozen=True)
 class LayerConfig:
-    """linear_graph.py:73-99, restricted to the recipes this build accelerates: quartet2
-    (rtn_1x16_46 + ms_eden), tetrajet_v2 (rtn_1x16 + sr_rht), nvidia (rtn_16x16 +
-    sr_rht, reused weights) and four_over_six (rtn_16x16_46 + sr_rht, reused weights)."""
+    """linear_graph.py:73-99.  ``posthoc`` (not in the reference) selects the
+    single-read post-hoc MS-EDEN schedule for the four backward quantizations."""
 
     forward_scheme: str = "rtn_1x16_46"
     backward_scheme: str = "ms_eden"
@@ -70,13 +74,49 @@ class LayerConfig:
             raise ValueError(f"unknown forward scheme {self.forward_scheme!r}")
         if self.backward_scheme not in BACKWARD_SCHEMES:
             raise ValueError(f"unknown backward scheme {self.backward_scheme!r}")
-        if self.ablation != "full":
+        if self.ablation not in ABLATIONS:
             raise ValueError(f"unknown ablation {self.ablation!r}")
-        if self.reuse_forward_weights and self.backward_scheme == "ms_eden":
-            raise ValueError("ms_eden requires weight re-quantization")
+        if self.backward_scheme == "ms_eden":
+            if self.ablation in ("b", "d"):
+                raise ValueError("ms_eden cannot quantize a single GEMM operand; "
+                                 f"ablation {self.ablation!r} is incompatible")
+            if self.reuse_forward_weights:
+                raise ValueError("ms_eden requires weight re-quantization")
         if self.reuse_forward_weights and not self.forward_scheme.startswith("rtn_16x16"):
-            # the reused 1x16 W^T is a dense (unquantized) GEMM operand in the reference
-            raise ValueError("reuse_forward_weights is built for the square-block weights only")
+            raise ValueError("weight reuse requires a square-block forward scheme")
+
+
+def format_config(cfg: LayerConfig) -> str:
+    """The key = value text form (linear_graph.py:153-159); ``posthoc`` is written only when set."""
+    text = (f"forward_scheme = {cfg.forward_scheme}\n"
+            f"backward_scheme = {cfg.backward_scheme}\n"
+            f"ablation = {cfg.ablation}\n"
+            f"reuse_forward_weights = {str(cfg.reuse_forward_weights).lower()}\n")
+    return text + ("posthoc = true\n" if cfg.posthoc else "")
+
+
+def parse_config(text: str) -> LayerConfig:
+    """Parse ``format_config`` text (linear_graph.py:162-182): '#' comments, blank lines,
+    unset keys default to the identity recipe; errors name the line."""
+    fields = {}
+    for lineno, raw in enumerate(text.splitlines(), 1):
+        line = raw.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if "=" not in line:
+            raise ValueError(f"config line {lineno}: expected key = value")
+        key, val = (part.strip() for part in line.split("=", 1))
+        if key in ("reuse_forward_weights", "posthoc"):
+            if val not in ("true", "false"):
+                raise ValueError(f"config line {lineno}: expected true/false")
+            fields[key] = val == "true"
+        elif key in ("forward_scheme", "backward_scheme", "ablation"):
+            fields[key] = val
+        else:
+            raise ValueError(f"config line {lineno}: unknown key {key!r}")
+    base = {"forward_scheme": "identity", "backward_scheme": "identity"}
+    base.update(fields)
+    return LayerConfig(**base)
 
 
 def baseline_config(name: str) -> LayerConfig:
@@ -93,8 +133,8 @@ def baseline_config(name: str) -> LayerConfig:
         return LayerConfig("rtn_16x16_46", "sr_46", reuse_forward_weights=True)
     if name == "identity":
         return LayerConfig("identity", "identity")
-    raise ValueError(f"unknown baseline {name!r}; known: ['quartet2', 'tetrajet_v2', 'nvidia', 'four_over_six', "
-                     f"'four_over_six_backward', 'identity']")
+    known = sorted(["quartet2", "tetrajet_v2", "nvidia", "four_over_six", "four_over_six_backward", "identity"])
+    raise ValueError(f"unknown baseline {name!r}; known: {known}")
 
 
 @dataclass
@@ -211,30 +251,58 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     main = torch.cuda.current_stream(e2.device)
     side = _side_stream(e2.device)
     side.wait_stream(main)
-    # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
+    # Ablation masks (linear_graph.py:296): operands outside the mask stay dense, and a
+    # GEMM with a dense operand runs as the reference's fp32 product of the dequantized
+    # values (cuBLAS); ms_eden needs both operands of a GEMM, SR rotates only when both
+    # are quantized (_sr_pair, linear_graph.py:259-274).
+    q_e, q_w, q_et, q_xt = ABLATION_MASK[cfg.ablation]
+    sr_scheme = cfg.backward_scheme != "ms_eden"
     sr_46 = cfg.backward_scheme in ("sr_46", "sr_rht_46")
-    if cfg.backward_scheme != "ms_eden":                # _sr_pair, linear_graph.py:259-274 via :310-326
-        rotate = cfg.backward_scheme in ("sr_rht", "sr_rht_46")
+    rht = cfg.backward_scheme in ("sr_rht", "sr_rht_46")
 
-        def quant(x, pair, operand, source):
-            return sr_operand(x, seeds, derive_stream(pair, operand), pair, source, rotate, sr_46, err)
-    else:                                               # ms_eden, linear_graph.py:304-307, :322-326
-        def quant(x, pair, operand, source):
-            return msed(x, seeds, 6.0, derive_stream(pair, operand), pair, mode, source, err)
+    def quant(x, pair, operand, source, both):
+        if sr_scheme:                                   # _sr_pair via linear_graph.py:310-331
+            return sr_operand(x, seeds, derive_stream(pair, operand), pair, source, rht and both, sr_46, err)
+        return msed(x, seeds, 6.0, derive_stream(pair, operand), pair, mode, source, err)   # :304-307, :322-326
+
+    def product(qa, qb, a_dense, b_dense, out_dtype):
+        """gemm_emulated(qa, qb): the NVFP4 GEMM when both operands are quantized, else
+        fp32 of the (dequantized) operands; a_dense/b_dense give the dense [M,K]/[N,K]."""
+        if qa is not None and qb is not None:
+            return gemm(qa, qb, out_dtype)
+        a = dequantize(qa).float() if qa is not None else a_dense()
+        b = dequantize(qb).float() if qb is not None else b_dense()
+        return torch.matmul(a, b.t()).to(out_dtype)
+
     with torch.cuda.stream(side):
-        qet = quant(e2, PAIR_DW, 0, "cols")
-        qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape")
-        dw = gemm(qet, qxt, torch.float32)
+        # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
+        if (q_et or q_xt) if sr_scheme else (q_et and q_xt):
+            both = q_et and q_xt
+            qet = quant(e2, PAIR_DW, 0, "cols", both) if q_et else None
+            qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape",
+                        both) if q_xt else None
+        else:
+            qet = qxt = None
+        if qet is None and qxt is None:
+            dw = torch.matmul(e2.float().t(), dense(tape.qX))
+        else:
+            dw = product(qet, qxt, lambda: e2.float().t(), lambda: dense(tape.qX).t(), torch.float32)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
     qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
-    if cfg.reuse_forward_weights:
+    qe = qwt = None
+    if cfg.reuse_forward_weights and q_w and sr_scheme:
         # saved square-block W^T goes in as is; E alone, SR without rotation (linear_graph.py:308-314)
-        qe = (quantize_sr_46 if sr_46 else quantize_sr)(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err)
+        qe = (quantize_sr_46 if sr_46 else quantize_sr)(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err) \
+            if q_e else None
         qwt = tape.qW.t
+    elif (q_e or q_w) if sr_scheme else (q_e and q_w):
+        both = q_e and q_w
+        qe = quant(e2, PAIR_DX, 0, "rows", both) if q_e else None
+        qwt = quant(qw, PAIR_DX, 1, "cols" if isinstance(qw, torch.Tensor) else "tape", both) if q_w else None
+    if qe is None and qwt is None:
+        dx = torch.matmul(e2.float(), dense(tape.qW)).to(dx_dtype)
     else:
-        qe = quant(e2, PAIR_DX, 0, "rows")
-        qwt = quant(qw, PAIR_DX, 1, "cols" if isinstance(qw, torch.Tensor) else "tape")
-    dx = gemm(qe, qwt, dx_dtype)
+        dx = product(qe, qwt, lambda: e2.float(), lambda: dense(tape.qW).t(), dx_dtype)
     main.wait_stream(side)
     _keep(main, dw)
     e2.record_stream(side)

@@ -22,6 +22,13 @@ from nvfp4emu import linear_graph as LG, ms_eden as ME, posthoc as PH, rht as RH
 from tests.families import FAMILIES, make  # noqa: E402
 
 
+ABLATION_CASES = [("ms_a", "rtn_1x16_46", "ms_eden", "a", False), ("ms_c", "rtn_1x16_46", "ms_eden", "c", False),
+                  ("ms_e", "rtn_1x16_46", "ms_eden", "e", False), ("rht_b", "rtn_1x16", "sr_rht", "b", False),
+                  ("rht_d", "rtn_1x16", "sr_rht", "d", False), ("sr46_a", "rtn_1x16_46", "sr_46", "a", False),
+                  ("nv_b", "rtn_16x16", "sr_rht", "b", True), ("nv_c", "rtn_16x16", "sr_rht", "c", True),
+                  ("nv_a", "rtn_16x16", "sr_rht", "a", True)]
+
+
 def pack(prefix, t, out):
     out[prefix + "fp4"] = t.fp4
     out[prefix + "s8"] = t.scales8
@@ -70,6 +77,11 @@ def main():
         y, tape = LG.forward(X, W, LG.baseline_config(name))
         g = LG.backward(tape, E, RH.SeedPair(7, 9))
         out.update({f"{tag}_Y": y, f"{tag}_dX": g.dX, f"{tag}_dW": g.dW})
+    # ablation masks (linear_graph.py:59-70, :296): (forward, backward, ablation, reuse)
+    for tag, fwd, bwd, abl, reuse in ABLATION_CASES:
+        y, tape = LG.forward(X, W, LG.LayerConfig(fwd, bwd, ablation=abl, reuse_forward_weights=reuse))
+        g = LG.backward(tape, E, RH.SeedPair(7, 9))
+        out.update({f"abl_{tag}_dX": g.dX, f"abl_{tag}_dW": g.dW})
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))

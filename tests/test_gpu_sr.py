@@ -6,6 +6,8 @@ tetrajet_v2 linear pass (rtn_1x16 forward, sr_rht backward).  Codes, scales
 and scale32 bit-exact; GEMM outputs within the tolerance of test_gpu_parity.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -188,6 +190,44 @@ def test_identity_schemes_linear(cuda, cfg_args):
         got = got.double().cpu().numpy()
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("fwd,bwd,abl,reuse,posthoc", [
+    ("rtn_1x16_46", "ms_eden", "a", False, False), ("rtn_1x16_46", "ms_eden", "c", False, True),
+    ("rtn_1x16_46", "ms_eden", "e", False, False), ("rtn_1x16", "sr_rht", "b", False, False),
+    ("rtn_1x16", "sr_rht", "d", False, False), ("rtn_1x16", "sr_rht", "a", False, False),
+    ("rtn_1x16_46", "sr_46", "b", False, False), ("rtn_1x16_46", "sr_rht_46", "c", False, False),
+    ("rtn_16x16", "sr_rht", "b", True, False), ("rtn_16x16", "sr_rht", "a", True, False),
+    ("rtn_16x16_46", "sr_46", "d", True, False), ("identity", "sr_rht", "d", False, False)])
+def test_ablation_masks_linear(cuda, fwd, bwd, abl, reuse, posthoc):
+    """Ablations a-e (linear_graph.py:59-70, :296): quantized operands bit-exact through the
+    oracle (pinned to the reference in test_oracle_pin), dense ones as fp32 products."""
+    q2 = _q2()
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.LayerConfig(fwd, bwd, ablation=abl, reuse_forward_weights=reuse, posthoc=posthoc)
+    y, tape = q2.forward(_dev(x), _dev(w), cfg)
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9))
+    ry, rtape = O.forward(x, w, forward_scheme=fwd)
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), backward_scheme=bwd, reuse_forward_weights=reuse,
+                          ablation=abl, posthoc=posthoc)
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        got = got.double().cpu().numpy()
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert rel < 1e-5, rel
+
+
+def test_ablation_golden_case(cuda):
+    """One ablation straight against the reference's own frozen output (tests/golden)."""
+    q2 = _q2()
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+    cfg = q2.LayerConfig("rtn_1x16_46", "ms_eden", ablation="a")
+    _, tape = q2.forward(_dev(gold["e2e_X"], False), _dev(gold["e2e_W"], False), cfg)   # fp32, as generated
+    g = q2.backward(tape, _dev(gold["e2e_E"], False), q2.SeedPair(7, 9))
+    for got, ref in ((g.dX, gold["abl_ms_a_dX"]), (g.dW, gold["abl_ms_a_dW"])):
+        got = got.double().cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
 
 
 def test_baseline_quantizer_errors(cuda):

@@ -104,3 +104,61 @@ def test_module_host_side():
     assert m.seeds_for(3) == q2.SeedPair(q2.derive_stream(5, 1, 3), q2.derive_stream(5, 2, 3))
     assert m.seeds_for(0) != q2.Quartet2Linear(256, 128, seed=6).seeds_for(0)
     assert "posthoc=True" in repr(m)
+
+
+def test_ablation_config_validation():
+    import paper_2601_22813_b200 as q2
+    for abl in q2.ABLATIONS:
+        q2.LayerConfig("rtn_1x16", "sr_rht", ablation=abl)
+    for abl in ("b", "d"):
+        with pytest.raises(ValueError, match="ms_eden cannot quantize a single GEMM operand"):
+            q2.LayerConfig(ablation=abl)
+    q2.LayerConfig(ablation="a"), q2.LayerConfig(ablation="c")
+    with pytest.raises(ValueError, match="unknown ablation"):
+        q2.LayerConfig(ablation="f")
+    with pytest.raises(ValueError, match="weight reuse requires a square-block forward scheme"):
+        q2.LayerConfig("rtn_1x16", "sr", reuse_forward_weights=True)
+    with pytest.raises(ValueError, match=r"known: \['four_over_six', 'four_over_six_backward', 'identity'"):
+        q2.baseline_config("quartet3")
+
+
+def test_config_text_round_trip():
+    import paper_2601_22813_b200 as q2
+    for name in ("quartet2", "nvidia", "four_over_six_backward", "identity"):
+        cfg = q2.baseline_config(name)
+        assert q2.parse_config(q2.format_config(cfg)) == cfg
+    cfg = q2.LayerConfig("rtn_1x16", "sr_rht", ablation="d", posthoc=True)
+    assert q2.parse_config(q2.format_config(cfg)) == cfg
+    assert q2.format_config(q2.baseline_config("nvidia")) == (
+        "forward_scheme = rtn_16x16\nbackward_scheme = sr_rht\nablation = full\nreuse_forward_weights = true\n")
+    assert q2.parse_config("# comment\n\nbackward_scheme = sr  # trailing\n") == q2.LayerConfig("identity", "sr")
+    for bad, msg in (("forward_scheme", "config line 1: expected key = value"),
+                     ("colour = red", "config line 1: unknown key 'colour'"),
+                     ("\nreuse_forward_weights = yes", "config line 2: expected true/false")):
+        with pytest.raises(ValueError, match=msg):
+            q2.parse_config(bad)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src"), reason="reference not mounted (GPU box)")
+def test_config_text_matches_live_reference(tmp_path):
+    import sys
+    os.environ.setdefault("NUMBA_CACHE_DIR", str(tmp_path))
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from nvfp4emu import linear_graph as LG
+    import paper_2601_22813_b200 as q2
+    for name in ("quartet2", "tetrajet_v2", "nvidia", "four_over_six", "four_over_six_backward", "identity"):
+        ref = LG.baseline_config(name)
+        assert q2.format_config(q2.baseline_config(name)) == LG.format_config(ref)
+        ours = q2.parse_config(LG.format_config(ref))
+        assert (ours.forward_scheme, ours.backward_scheme, ours.ablation, ours.reuse_forward_weights) == \
+            (ref.forward_scheme, ref.backward_scheme, ref.ablation, ref.reuse_forward_weights)
+    for text in ("ablation = b", "ablation = b\nbackward_scheme = sr", "reuse_forward_weights = true",
+                 "forward_scheme = rtn_16x16\nbackward_scheme = ms_eden\nreuse_forward_weights = true"):
+        outcomes = []
+        for parse in (LG.parse_config, q2.parse_config):
+            try:
+                c = parse(text)
+                outcomes.append((c.forward_scheme, c.backward_scheme, c.ablation, c.reuse_forward_weights))
+            except ValueError as exc:
+                outcomes.append(str(exc))
+        assert outcomes[0] == outcomes[1], (text, outcomes)
