@@ -45,7 +45,7 @@ extern "C" {
 #endif
 
 enum { Q2_OK = 0, Q2_EINVAL = 1, Q2_ECUDA = 2 };
-enum { Q2_BF16 = 0, Q2_F32 = 1 };
+enum { Q2_BF16 = 0, Q2_F32 = 1, Q2_F64 = 2 };   /* Q2_F64: q2_rht input only */
 
 /* err-word bits (device uint32) */
 enum {
@@ -209,6 +209,15 @@ int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_dtype, int64
 int q2_dequant(const q2_nvfp4* t, double* out, void* stream);
 int q2_unpack(const q2_nvfp4* t, uint8_t* fp4, uint8_t* scales8, void* stream);
 int q2_pack(const uint8_t* fp4, const uint8_t* scales8, const q2_nvfp4* t, void* stream);
+
+/* Chunked randomized Hadamard in literal float64: rht_apply (rht.py:144-155),
+ * rht_inverse (:158-163) and hadamard_128 (:121-130).  x: n elements (BF16, F32
+ * or F64), n % chunk == 0, chunk a power of two in [16, 2048].  Per chunk
+ * out = FWHT(x * signs_pre) * scale * signs_post (either sign vector may be
+ * NULL; chunk doubles of +-1), butterflies in the reference order
+ * (_kernels.py:175-187), so out equals the reference bit for bit.  out: n f64.  */
+int q2_rht(const void* x, int dtype, int64_t n, int chunk, const double* signs_pre, const double* signs_post,
+           double scale, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -5,7 +5,7 @@ Drop-in for the hot path of the reference emulator ``nvfp4emu``
 meanings, computed by hand-written sm_100a CUDA in ``libquartet2.so``.
 """
 
-from .rht import CHUNK, SeedPair, derive_stream, prng_uniform, sign_mask
+from .rht import CHUNK, SeedPair, derive_stream, hadamard_128, prng_signs, prng_uniform, rht_apply, rht_inverse, sign_mask
 from .quantizers import (GROUP, absmax, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
                          deserialize_nvfp4, quantize_rtn, quantize_rtn_46, serialize_nvfp4, set_error_mode)
 from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
@@ -24,4 +24,5 @@ __all__ = [
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
     "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
     "Quartet2Linear", "Quartet2LinearFunction", "quartet2_linear", "ABLATIONS", "format_config", "parse_config",
+    "prng_signs", "rht_apply", "rht_inverse", "hadamard_128",
 ]

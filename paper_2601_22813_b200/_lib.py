@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libquartet2.so")
 
 Q2_OK, Q2_EINVAL, Q2_ECUDA = 0, 1, 2
-Q2_BF16, Q2_F32 = 0, 1
+Q2_BF16, Q2_F32, Q2_F64 = 0, 1, 2
 Q2_SRC_ROWS, Q2_SRC_COLS, Q2_SRC_TAPE_COLS = 0, 1, 2
 Q2_MSED_EXACT, Q2_MSED_POW2, Q2_MSED_POSTHOC = 0, 1, 2
 Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF, Q2_ERR_SR_CLIP = 1, 2, 4, 8, 16
@@ -25,6 +25,7 @@ EXPORTS = (
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
     "q2_msed_dual_posthoc", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
     "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant", "q2_quant_square_block", "q2_sr_quant_src", "q2_quant_fwd_amax",
+    "q2_rht",
 )
 
 
@@ -67,6 +68,7 @@ _SIGS = {
     "q2_dequant": (_I, [_TP, _P, _P]),
     "q2_unpack": (_I, [_TP, _P, _P, _P]),
     "q2_pack": (_I, [_P, _P, _TP, _P]),
+    "q2_rht": (_I, [_P, _I, _I64, _I, _P, _P, _D, _P, _P]),
 }
 
 

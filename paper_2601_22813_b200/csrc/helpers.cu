@@ -47,9 +47,68 @@ __global__ void pack_kernel(const uint8_t* __restrict__ fp4, const uint8_t* __re
   *reinterpret_cast<uint2*>(codes + r * (K / 2) + j * 8) = make_uint2(lo, hi);
 }
 
+// Chunked randomized Hadamard in literal float64 (rht_apply / rht_inverse /
+// hadamard_128, rht.py:121-163; butterflies _kernels.py:175-187): per chunk,
+// out = FWHT(x * pre) * c * post, stages h = 1, 2, ..., chunk/2, every output one
+// IEEE op (a + b or a - b) of two stage inputs, so the bits equal the reference's.
+// A block transforms a tile of 2 * blockDim.x elements (whole chunks) in shared
+// memory; each thread owns one butterfly pair per stage.
+template <int DT>
+__global__ void rht_kernel(const void* __restrict__ x, int64_t total, int chunk, const double* __restrict__ pre,
+                           const double* __restrict__ post, double c, double* __restrict__ out) {
+  extern __shared__ double tile_sh[];
+  const int tile = 2 * blockDim.x;
+  const int64_t base = (int64_t)blockIdx.x * tile;
+  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+    const int64_t g = base + i;
+    double v = 0.0;
+    if (g < total)
+      v = DT == Q2_BF16 ? (double)bf16_to_f32(static_cast<const uint16_t*>(x)[g])
+          : DT == Q2_F32 ? (double)static_cast<const float*>(x)[g]
+                         : static_cast<const double*>(x)[g];
+    if (pre) v = __dmul_rn(v, pre[i & (chunk - 1)]);
+    tile_sh[i] = v;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  for (int h = 1; h < chunk; h <<= 1) {
+    const int i = (t / h) * 2 * h + (t % h), j = i + h;
+    const double a = tile_sh[i], b = tile_sh[j];
+    tile_sh[i] = __dadd_rn(a, b);
+    tile_sh[j] = __dsub_rn(a, b);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < tile; i += blockDim.x) {
+    const int64_t g = base + i;
+    if (g >= total) continue;
+    double v = __dmul_rn(tile_sh[i], c);
+    if (post) v = __dmul_rn(v, post[i & (chunk - 1)]);
+    out[g] = v;
+  }
+}
+
 }  // namespace q2
 
 using namespace q2;
+
+extern "C" int q2_rht(const void* x, int dtype, int64_t n, int chunk, const double* signs_pre,
+                      const double* signs_post, double scale, double* out, void* stream) {
+  if (chunk < 16 || (chunk & (chunk - 1)) || chunk > 2048 || n % chunk) return Q2_EINVAL;
+  if (n == 0) return Q2_OK;
+  if (!x || !out || (dtype != Q2_BF16 && dtype != Q2_F32 && dtype != Q2_F64)) return Q2_EINVAL;
+  const int tile = std::max(chunk, 512), threads = tile / 2;
+  const unsigned blocks = (unsigned)((n + tile - 1) / tile);
+  const size_t smem = (size_t)tile * sizeof(double);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto launch = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<blocks, threads, smem, s>>>(x, n, chunk, signs_pre, signs_post, scale, out);
+  };
+  if (dtype == Q2_BF16) launch(rht_kernel<Q2_BF16>);
+  else if (dtype == Q2_F32) launch(rht_kernel<Q2_F32>);
+  else launch(rht_kernel<Q2_F64>);
+  return cudaGetLastError() == cudaSuccess ? Q2_OK : Q2_ECUDA;
+}
 
 static unsigned nblocks(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + 255) / 256); }
 

@@ -82,6 +82,11 @@ def main():
         y, tape = LG.forward(X, W, LG.LayerConfig(fwd, bwd, ablation=abl, reuse_forward_weights=reuse))
         g = LG.backward(tape, E, RH.SeedPair(7, 9))
         out.update({f"abl_{tag}_dX": g.dX, f"abl_{tag}_dW": g.dW})
+    # rotations (rht.py:121-163) on wide-range fp32 rows
+    rx = (rng.standard_normal((6, 512)) * np.exp(rng.normal(0, 4, (6, 512)))).astype(np.float32)
+    out.update(rot_x=rx, rot_apply128=RH.rht_apply(rx, 11, RH.derive_stream(1)),
+               rot_apply32=RH.rht_apply(rx, 11, 5, chunk=32), rot_apply512=RH.rht_apply(rx, 3, 0, chunk=512),
+               rot_inv128=RH.rht_inverse(rx, 11, RH.derive_stream(1)), rot_h128=RH.hadamard_128(rx.reshape(-1, 128)))
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))
