@@ -199,3 +199,61 @@ def pass2(er: ErNvfp4Tensor, red: Pass1Reductions, seed_sr: int, tensor_id: int 
     _lib.check(rc, "posthoc pass2")
     _finish(err)
     return out
+
+
+@dataclass(frozen=True)
+class KernelCost:
+    """Traffic of one kernel of a re-quantization pipeline (posthoc.py:128-132)."""
+
+    gmem_to_sm_bits_per_elem: float
+    sm_to_gmem_bits_per_elem: float
+    mma_calls_per_group: int
+
+
+@dataclass(frozen=True)
+class CostReport:
+    """Both kernels of a pipeline and their totals (posthoc.py:135-155)."""
+
+    pipeline: str
+    kernel1: KernelCost
+    kernel2: KernelCost
+
+    @property
+    def gmem_to_sm_total(self) -> float:
+        return self.kernel1.gmem_to_sm_bits_per_elem + self.kernel2.gmem_to_sm_bits_per_elem
+
+    @property
+    def sm_to_gmem_total(self) -> float:
+        return self.kernel1.sm_to_gmem_bits_per_elem + self.kernel2.sm_to_gmem_bits_per_elem
+
+    @property
+    def mma_total(self) -> int:
+        return self.kernel1.mma_calls_per_group + self.kernel2.mma_calls_per_group
+
+    @property
+    def total_bits_per_elem(self) -> float:
+        return self.gmem_to_sm_total + self.sm_to_gmem_total
+
+
+def cost_model(pipeline: str, elem_bits: int = 4, scale_bits: int = 8, pseudo_scale_bits: int = 16,
+               group: int = GROUP) -> CostReport:
+    """Bits moved per element by the naive (absmax pass + quantize pass) and the
+    post-hoc (one read writing the extended-range form, then a scales-only pass)
+    re-quantization of an NVFP4 tensor (posthoc.py:158-188).  The B200 post-hoc
+    kernels (``msed64_kernel<…, POSTHOC>`` + ``msed64_pass2_kernel``) follow the
+    post-hoc schedule; their pass 1 also writes one float64 EDEN factor per
+    128-chunk (0.5 bit/elem) that this model, like the reference's, leaves out."""
+    nvfp4 = elem_bits + scale_bits / group
+    er = elem_bits + pseudo_scale_bits / group
+    if pipeline == "naive":
+        return CostReport("naive", KernelCost(nvfp4, 0.0, 1), KernelCost(nvfp4, nvfp4, 1))
+    if pipeline == "posthoc":
+        return CostReport("posthoc", KernelCost(nvfp4, er, 1),
+                          KernelCost(pseudo_scale_bits / group, scale_bits / group, 0))
+    raise ValueError(f"unknown pipeline {pipeline!r}; expected 'naive' or 'posthoc'")
+
+
+def cost_model_table() -> dict:
+    """Both pipelines and the relative bandwidth saving (posthoc.py:191-199)."""
+    naive, post = cost_model("naive"), cost_model("posthoc")
+    return {"naive": naive, "posthoc": post, "saving": 1.0 - post.total_bits_per_elem / naive.total_bits_per_elem}

@@ -162,3 +162,23 @@ def test_config_text_matches_live_reference(tmp_path):
             except ValueError as exc:
                 outcomes.append(str(exc))
         assert outcomes[0] == outcomes[1], (text, outcomes)
+
+
+def test_cost_model():
+    """posthoc.py:158-199: naive 4.5 + (4.5 + 4.5) bits/elem, post-hoc (4.5 + 5) + (1 + 0.5)."""
+    import paper_2601_22813_b200 as q2
+    t = q2.cost_model_table()
+    assert t["naive"].total_bits_per_elem == 13.5 and t["naive"].mma_total == 2
+    assert t["posthoc"].total_bits_per_elem == 11.0 and t["posthoc"].mma_total == 1
+    assert abs(t["saving"] - (1 - 11 / 13.5)) < 1e-15
+    with pytest.raises(ValueError, match="expected 'naive' or 'posthoc'"):
+        q2.cost_model("eager")
+    if os.path.isdir("/root/reference/pkg/src"):
+        import sys
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from nvfp4emu import posthoc as PH
+        for args in ((), (4, 8, 16, 32), (2, 8, 8, 16)):
+            for pipe in ("naive", "posthoc"):
+                a, b = q2.cost_model(pipe, *args), PH.cost_model(pipe, *args)
+                assert (a.total_bits_per_elem, a.mma_total, a.gmem_to_sm_total) == \
+                    (b.total_bits_per_elem, b.mma_total, b.gmem_to_sm_total)
