@@ -182,3 +182,16 @@ def test_cost_model():
                 a, b = q2.cost_model(pipe, *args), PH.cost_model(pipe, *args)
                 assert (a.total_bits_per_elem, a.mma_total, a.gmem_to_sm_total) == \
                     (b.total_bits_per_elem, b.mma_total, b.gmem_to_sm_total)
+
+
+def test_reports_to_json_stable():
+    import json
+    import numpy as np
+    from paper_2601_22813_b200 import harness as H
+    r = H.MseReport("quartet2", "1x16", np.float64(1.5e-3), 1e-6, 1000, 0)
+    text = H.reports_to_json({"mse": [r], "slope": np.float32(-1.0), "b": np.arange(3)})
+    assert text == H.reports_to_json({"b": np.arange(3), "slope": np.float32(-1.0), "mse": [r]})
+    d = json.loads(text)
+    assert d["mse"][0]["mse_e3"] == 1.5 and d["b"] == [0, 1, 2] and text.endswith("\n")
+    with pytest.raises(TypeError, match="not JSON-serializable"):
+        H.reports_to_json({"x": object()})
