@@ -219,6 +219,14 @@ int q2_pack(const uint8_t* fp4, const uint8_t* scales8, const q2_nvfp4* t, void*
 int q2_rht(const void* x, int dtype, int64_t n, int chunk, const double* signs_pre, const double* signs_post,
            double scale, double* out, void* stream);
 
+/* Element formats (formats.py:76-229) over n float64 inputs / uint8 codes:
+ * op 0 encode_fp4_rtn, 1 encode_fp4_sr (u), 2 encode_fp8_rtn, 3 encode_fp8_sr (u),
+ * 4 round_e8m3_rtn (vals_out; overflow sets Q2_ERR_E8M3_OVF in err),
+ * 5 decode_fp4 (codes_in 0..15), 6 decode_fp8 (codes_in 0..255).
+ * The caller has applied the reference's input checks (NaN, negative, grid max). */
+int q2_formats(int op, const double* x, const double* u, const uint8_t* codes_in, int64_t n, uint8_t* codes_out,
+               double* vals_out, uint32_t* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@ from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_
 from .linear_graph import (ABLATIONS, GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config,
                            format_config, forward, gemm, gemm_emulated, parse_config)
 from .module import Quartet2Linear, Quartet2LinearFunction, quartet2_linear
+from . import formats  # noqa: F401  (formats.py mirror: encode_fp4_rtn, ..., decode_fp8)
 
 __all__ = [
     "CHUNK", "GROUP", "GUARDED_SCALE_CAP", "FP8_RTN_MARGIN", "SeedPair", "derive_stream", "prng_uniform",

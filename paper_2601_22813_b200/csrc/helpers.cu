@@ -87,9 +87,76 @@ __global__ void rht_kernel(const void* __restrict__ x, int64_t total, int chunk,
   }
 }
 
+// Element formats (formats.py:85-229) as one elementwise kernel over float64
+// inputs; every op is the device helper the quantizers use (common.cuh), so the
+// standalone encoders equal the fused ones.  Input checks the reference raises
+// for (NaN, negative, above the grid) are done by the host wrapper before launch.
+enum { FMT_FP4_RTN = 0, FMT_FP4_SR = 1, FMT_FP8_RTN = 2, FMT_FP8_SR = 3, FMT_E8M3 = 4, FMT_DEC_FP4 = 5,
+       FMT_DEC_FP8 = 6 };
+
+__device__ __forceinline__ uint32_t fp4_code_of_doubled(double r) {  // doubled grid 0,1,2,3,4,6,8,12 -> 0..7
+  const uint32_t ri = (uint32_t)r;
+  return ri <= 4u ? ri : (ri == 6u ? 5u : (ri == 8u ? 6u : 7u));
+}
+
+__global__ void formats_kernel(int op, const double* __restrict__ x, const double* __restrict__ u,
+                               const uint8_t* __restrict__ cin, int64_t n, uint8_t* __restrict__ cout,
+                               double* __restrict__ vout, uint32_t* __restrict__ err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    switch (op) {
+      case FMT_FP4_RTN:                                                   // formats.py:116-124
+        cout[i] = (uint8_t)rtn_code_literal(x[i], 1.0);
+        break;
+      case FMT_FP4_SR: {                                                  // formats.py:127-157
+        const double v = x[i], a2 = fmin(fabs(v) * 2.0, 12.0);
+        const double lo = a2 < 4.0 ? floor(a2) : (a2 < 8.0 ? 2.0 * floor(a2 * 0.5) : 4.0 * floor(a2 * 0.25));
+        const double step = lo < 4.0 ? 1.0 : (lo < 8.0 ? 2.0 : 4.0);
+        const double p = __ddiv_rn(__dsub_rn(a2, lo), step);
+        const double r = u[i] < p ? lo + step : lo;
+        cout[i] = (uint8_t)(fp4_code_of_doubled(r) | (signbit(v) ? 8u : 0u));
+        break;
+      }
+      case FMT_FP8_RTN:                                                   // formats.py:160-171
+        cout[i] = (uint8_t)e4m3_rtn(x[i]);
+        break;
+      case FMT_FP8_SR:                                                    // formats.py:174-201
+        cout[i] = (uint8_t)e4m3_sr(x[i], u[i]);
+        break;
+      case FMT_E8M3: {                                                    // formats.py:204-229
+        bool ovf = false;
+        vout[i] = e8m3_rtn(x[i], &ovf);
+        if (ovf) atomic_or_err(err, Q2_ERR_E8M3_OVF);
+        break;
+      }
+      case FMT_DEC_FP4:                                                   // formats.py:76-78
+        vout[i] = fp4_val(cin[i]);
+        break;
+      default: {                                                          // FMT_DEC_FP8, formats.py:81-83
+        const uint32_t c = cin[i];
+        double v = (c & 0x7Fu) == 0x7Fu ? __longlong_as_double(0x7FF8000000000000ll) : e4m3_val(c & 0x7Fu);
+        vout[i] = (c & 0x80u) ? -v : v;
+      }
+    }
+  }
+}
+
 }  // namespace q2
 
 using namespace q2;
+
+extern "C" int q2_formats(int op, const double* x, const double* u, const uint8_t* codes_in, int64_t n,
+                          uint8_t* codes_out, double* vals_out, uint32_t* err, void* stream) {
+  if (op < FMT_FP4_RTN || op > FMT_DEC_FP8 || n < 0) return Q2_EINVAL;
+  if (n == 0) return Q2_OK;
+  const bool decode = op >= FMT_DEC_FP4, vals = decode || op == FMT_E8M3;
+  if ((decode ? !codes_in : !x) || (vals ? !vals_out : !codes_out) || ((op == FMT_FP4_SR || op == FMT_FP8_SR) && !u) ||
+      (op == FMT_E8M3 && !err))
+    return Q2_EINVAL;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  formats_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(op, x, u, codes_in, n, codes_out, vals_out,
+                                                                        err);
+  return cudaGetLastError() == cudaSuccess ? Q2_OK : Q2_ECUDA;
+}
 
 extern "C" int q2_rht(const void* x, int dtype, int64_t n, int chunk, const double* signs_pre,
                       const double* signs_post, double scale, double* out, void* stream) {

@@ -87,6 +87,25 @@ def main():
     out.update(rot_x=rx, rot_apply128=RH.rht_apply(rx, 11, RH.derive_stream(1)),
                rot_apply32=RH.rht_apply(rx, 11, 5, chunk=32), rot_apply512=RH.rht_apply(rx, 3, 0, chunk=512),
                rot_inv128=RH.rht_inverse(rx, 11, RH.derive_stream(1)), rot_h128=RH.hadamard_128(rx.reshape(-1, 128)))
+    # element formats (formats.py:76-229) on grid points, exact midpoints/ties and random values
+    from nvfp4emu import formats as F
+    g4 = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+    x4 = np.concatenate([g4, -g4, (g4[:-1] + g4[1:]) / 2, -(g4[:-1] + g4[1:]) / 2, [-0.0, 6.0000000001, 7.5, np.inf],
+                         rng.standard_normal(300) * 2.5]).astype(np.float64)
+    x4sr = np.clip(x4, -6.0, 6.0)
+    u4 = rng.random(x4.size)
+    p8 = F.E4M3_VALUES[:127]
+    x8 = np.concatenate([p8, (p8[:-1] + p8[1:]) / 2, [0.0, 2.0 ** -10, 2.0 ** -6 * 0.99, 440.0, 448.0, 500.0, np.inf],
+                         np.exp(rng.normal(-2, 3, 300))]).astype(np.float64)
+    x8sr = np.minimum(x8, 448.0)
+    u8 = rng.random(x8.size)
+    xe = np.concatenate([[0.0, 2.0 ** -126, 2.0 ** -127, 2.0 ** -127 * 1.01, 1.0625, 1.1875, 3.0e38],
+                         np.exp(rng.normal(0, 20, 300))]).astype(np.float64)
+    out.update(fmt_x4=x4, fmt_x4sr=x4sr, fmt_u4=u4, fmt_fp4_rtn=F.encode_fp4_rtn(x4),
+               fmt_fp4_sr=F.encode_fp4_sr(x4sr, u4), fmt_x8=x8, fmt_x8sr=x8sr, fmt_u8=u8,
+               fmt_fp8_rtn=F.encode_fp8_rtn(x8), fmt_fp8_sr=F.encode_fp8_sr(x8sr, u8), fmt_xe=xe,
+               fmt_e8m3=F.round_e8m3_rtn(xe), fmt_dec_fp4=F.decode_fp4(np.arange(16)),
+               fmt_dec_fp8=F.decode_fp8(np.arange(256)))
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))
