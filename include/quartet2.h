@@ -227,6 +227,11 @@ int q2_rht(const void* x, int dtype, int64_t n, int chunk, const double* signs_p
 int q2_formats(int op, const double* x, const double* u, const uint8_t* codes_in, int64_t n, uint8_t* codes_out,
                double* vals_out, uint32_t* err, void* stream);
 
+/* EDEN correction factors (chunk_correction_factors, ms_eden.py:75-83): for each of
+ * nchunks contiguous 128-element float64 chunks, S = sum(x_rot^2) / sum(x_rot*x_rtn)
+ * in numpy's summation order, 1.0 when degenerate.  out: nchunks doubles.         */
+int q2_eden_factors(const double* x_rot, const double* x_rtn, int64_t nchunks, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,9 +140,45 @@ __global__ void formats_kernel(int op, const double* __restrict__ x, const doubl
   }
 }
 
+// EDEN correction factors per 128-chunk (chunk_correction_factors,
+// ms_eden.py:75-83): num = sum(x_rot^2), den = sum(x_rot * x_rtn) with the
+// products materialised and summed in numpy's order for a contiguous 128-row
+// (8 strided accumulators, sequential; then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// SURVEY §8(c) E7); S = num/den unless num == 0 or |den| < 1e-30 num.  One thread
+// per chunk (an API helper; the quantizers fuse this step).
+__device__ __forceinline__ double np_sum128_products(const double* a, const double* b) {
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = __dmul_rn(a[j], b[j]);
+  for (int k = 1; k < 16; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __dmul_rn(a[8 * k + j], b[8 * k + j]));
+  return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+}
+
+__global__ void eden_factor_kernel(const double* __restrict__ xr, const double* __restrict__ xq, int64_t nchunks,
+                                   double* __restrict__ out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const double* a = xr + c * 128;
+  const double num = np_sum128_products(a, a), den = np_sum128_products(a, xq + c * 128);
+  const bool good = fabs(den) >= 1e-30 * num && num > 0.0;
+  out[c] = good ? __ddiv_rn(num, den) : 1.0;
+}
+
 }  // namespace q2
 
 using namespace q2;
+
+extern "C" int q2_eden_factors(const double* x_rot, const double* x_rtn, int64_t nchunks, double* out, void* stream) {
+  if (nchunks < 0) return Q2_EINVAL;
+  if (nchunks == 0) return Q2_OK;
+  if (!x_rot || !x_rtn || !out) return Q2_EINVAL;
+  eden_factor_kernel<<<(unsigned)((nchunks + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(x_rot, x_rtn,
+                                                                                                      nchunks, out);
+  return cudaGetLastError() == cudaSuccess ? Q2_OK : Q2_ECUDA;
+}
 
 extern "C" int q2_formats(int op, const double* x, const double* u, const uint8_t* codes_in, int64_t n,
                           uint8_t* codes_out, double* vals_out, uint32_t* err, void* stream) {

@@ -13,6 +13,8 @@ saved NVFP4 tape tensor (W^T, X^T of linear_graph.py:293-294, 304, 322-323).
 from __future__ import annotations
 
 import ctypes
+
+import numpy as np
 from dataclasses import dataclass
 
 import torch
@@ -257,3 +259,42 @@ def cost_model_table() -> dict:
     """Both pipelines and the relative bandwidth saving (posthoc.py:191-199)."""
     naive, post = cost_model("naive"), cost_model("posthoc")
     return {"naive": naive, "posthoc": post, "saving": 1.0 - post.total_bits_per_elem / naive.total_bits_per_elem}
+
+
+@dataclass
+class CorrectionFactors:
+    """Per-128-chunk rescaling factors (ms_eden.py:50-54)."""
+
+    per_chunk: "torch.Tensor"
+
+
+def _f64_device(x) -> torch.Tensor:
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(np.asarray(x, dtype=np.float64))
+    return (x if x.is_cuda else x.cuda()).to(torch.float64).contiguous()
+
+
+def chunk_correction_factors(x_rot, x_rtn) -> torch.Tensor:
+    """EDEN factors S = <x,x>/<x,q> for every 128-chunk of the last axis, 1.0 when
+    degenerate (ms_eden.py:75-83), in numpy's summation order: a float64 CUDA
+    tensor [..., K/128] equal to the reference bit for bit."""
+    xr, xq = _f64_device(x_rot), _f64_device(x_rtn)
+    if xr.shape != xq.shape or xr.dim() == 0 or xr.shape[-1] % CHUNK:
+        raise ValueError(f"chunk_correction_factors expects matching shapes with the last dimension a multiple of "
+                         f"{CHUNK}")
+    out = torch.empty(*xr.shape[:-1], xr.shape[-1] // CHUNK, dtype=torch.float64, device=xr.device)
+    n = out.numel()
+    rc = _lib.lib().q2_eden_factors(xr.data_ptr() if n else None, xq.data_ptr() if n else None, n,
+                                    out.data_ptr() if n else None, stream_handle())
+    _lib.check(rc, "q2_eden_factors")
+    return out
+
+
+def correction_factor(x_rot, x_rtn) -> float:
+    """Factor of one 128-element chunk (ms_eden.py:57-72).  The reference forms the two
+    dot products with BLAS (``@``), whose summation order is the BLAS build's; this
+    uses numpy's pairwise ``.sum`` order, so results agree to rounding, not bits."""
+    xr, xq = _f64_device(x_rot), _f64_device(x_rtn)
+    if xr.shape != xq.shape or xr.shape[-1] != CHUNK or xr.dim() != 1:
+        raise ValueError(f"correction_factor expects matching length-{CHUNK} chunks")
+    return float(chunk_correction_factors(xr, xq)[0])

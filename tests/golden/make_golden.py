@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import nvfp4emu as R  # noqa: E402
-from nvfp4emu import linear_graph as LG, ms_eden as ME, posthoc as PH, rht as RH  # noqa: E402
+from nvfp4emu import linear_graph as LG, ms_eden as ME, posthoc as PH, quantizers as Q, rht as RH  # noqa: E402
 
 from tests.families import FAMILIES, make  # noqa: E402
 
@@ -106,6 +106,15 @@ def main():
                fmt_fp8_rtn=F.encode_fp8_rtn(x8), fmt_fp8_sr=F.encode_fp8_sr(x8sr, u8), fmt_xe=xe,
                fmt_e8m3=F.round_e8m3_rtn(xe), fmt_dec_fp4=F.decode_fp4(np.arange(16)),
                fmt_dec_fp8=F.decode_fp8(np.arange(256)))
+    # EDEN correction factors (ms_eden.py:57-83) on a rotated wide-range tensor, with
+    # an all-zero chunk and a chunk whose quantization is zero (degenerate den)
+    xf = (rng.standard_normal((8, 512)) * np.exp(rng.normal(0, 3, (8, 1)))).astype(np.float32).astype(np.float64)
+    xf[2, 128:256] = 0.0
+    xr = RH.rht_apply(xf, 5, 9)
+    xr[5, 256:384] = xr[5, 256:384] * 1e-30
+    xq = Q.dequantize(Q.quantize_rtn(xr))
+    out.update(eden_xrot=xr, eden_xrtn=xq, eden_S=ME.chunk_correction_factors(xr, xq),
+               eden_S1=np.array([ME.correction_factor(xr[0, :128], xq[0, :128])]))
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))

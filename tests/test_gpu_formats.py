@@ -63,3 +63,18 @@ def test_format_errors(cuda):
     with pytest.raises(IndexError):
         F.decode_fp4([16])
     assert F.encode_fp8_rtn(np.zeros(0)).numel() == 0
+
+
+def test_eden_correction_factors_golden(cuda):
+    """chunk_correction_factors (ms_eden.py:75-83) bit-exact incl. degenerate chunks;
+    correction_factor (:57-72, a BLAS dot in the reference) to rounding."""
+    import paper_2601_22813_b200 as q2
+    S = q2.ms_eden.chunk_correction_factors(GOLD["eden_xrot"], GOLD["eden_xrtn"])
+    assert S.shape == (8, 4) and S.dtype == torch.float64
+    np.testing.assert_array_equal(_np(S), GOLD["eden_S"])
+    s1 = q2.ms_eden.correction_factor(GOLD["eden_xrot"][0, :128], GOLD["eden_xrtn"][0, :128])
+    assert abs(s1 - GOLD["eden_S1"][0]) <= 1e-14 * abs(GOLD["eden_S1"][0])
+    with pytest.raises(ValueError, match="correction_factor expects matching length-128 chunks"):
+        q2.ms_eden.correction_factor(np.ones(64), np.ones(64))
+    with pytest.raises(ValueError, match="chunk_correction_factors expects matching shapes"):
+        q2.ms_eden.chunk_correction_factors(np.ones((2, 256)), np.ones((2, 128)))
