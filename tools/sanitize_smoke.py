@@ -34,6 +34,19 @@ def main():
     q2.ms_eden_quantize(xf, q2.SeedPair(1, 2), tensor_id=5, pow2_scale=True)
     t = q2.quantize_rtn_46(xf)
     assert q2.deserialize_nvfp4(q2.serialize_nvfp4(t)).to_reference()[2] == t.to_reference()[2]
+    # standalone ops: rotations, formats, EDEN factors, ablation masks
+    r = q2.rht_apply(xf, 3, 4, chunk=256)
+    q2.rht_inverse(r, 3, 4, chunk=256)
+    q2.hadamard_128(xf[:, :128])
+    from paper_2601_22813_b200 import formats as F
+    F.encode_fp4_rtn(xf), F.encode_fp4_sr(xf.clamp(-6, 6), torch.rand_like(xf))
+    F.encode_fp8_rtn(xf.abs()), F.encode_fp8_sr(xf.abs().clamp(max=448), torch.rand_like(xf))
+    F.round_e8m3_rtn(xf.abs()), F.decode_fp4(torch.arange(16)), F.decode_fp8(torch.arange(256))
+    q2.ms_eden.chunk_correction_factors(r, r * 0.5)
+    for abl in ("a", "b", "c", "d"):
+        cfg = q2.LayerConfig("rtn_1x16", "sr_rht", ablation=abl)
+        y, tape = q2.forward(X, W, cfg)
+        q2.backward(tape, E, q2.SeedPair(3, 4))
     m = q2.Quartet2Linear(256, 128, bias=True, device="cuda")
     m(X).float().sum().backward()
     torch.cuda.synchronize()
