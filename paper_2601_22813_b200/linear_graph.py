@@ -171,11 +171,30 @@ def gemm(qa: NVFP4Tensor, qb: NVFP4Tensor, out_dtype=torch.float32, out: torch.T
     return out
 
 
+def _dense64(t) -> torch.Tensor:
+    if isinstance(t, (NVFP4Tensor, SquareBlockTensor)):
+        return dequantize(t)
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    return (t if t.is_cuda else t.cuda()).to(torch.float64)
+
+
 def gemm_emulated(qa, qb, accumulate: str = "f32") -> torch.Tensor:
-    """Name-compatible entry for linear_graph.gemm_emulated: FP32-accumulated NVFP4 GEMM."""
-    if accumulate != "f32":
+    """linear_graph.gemm_emulated (linear_graph.py:190-205): ``"f32"`` runs the tcgen05
+    NVFP4 GEMM when both operands are NVFP4 (an FP32 product of the dequantized values
+    when one is a plain tensor); ``"f64"`` is the float64 product of the dequantized
+    operands (cuBLAS DGEMM), the reference's oracle mode."""
+    if accumulate not in ("f32", "f64"):
         raise ValueError(f"unknown accumulate precision {accumulate!r}")
-    return gemm(qa, qb, torch.float32)
+    quantized = isinstance(qa, NVFP4Tensor) and isinstance(qb, NVFP4Tensor)
+    if accumulate == "f32" and quantized:
+        return gemm(qa, qb, torch.float32)
+    a, b = _dense64(qa), _dense64(qb)
+    if a.shape[-1] != b.shape[-1]:
+        raise ValueError(f"inner dimensions disagree: {tuple(a.shape)} vs {tuple(b.shape)}")
+    if accumulate == "f64":
+        return a @ b.t()
+    return a.float() @ b.float().t()
 
 
 def _check_dims(x_shape, w_shape, cfg: LayerConfig) -> None:
@@ -206,8 +225,11 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     w2, ws, _ = as_device_matrix(w, "W")
     _check_dims(xs, ws, cfg)
     caps = (6.0, 4.0) if cfg.forward_scheme.endswith("_46") else (6.0,)   # linear_graph.py:208-221
+    if accumulate not in ("f32", "f64"):
+        raise ValueError(f"unknown accumulate precision {accumulate!r}")
     if cfg.forward_scheme == "identity":              # unquantized: plain FP32 GEMM (cuBLAS), linear_graph.py:208-210
-        y = torch.matmul(x2.float(), w2.float().t()).to(out_dtype)
+        y = gemm_emulated(x2, w2, accumulate)
+        y = y.to(out_dtype) if accumulate == "f32" else y
         return y, LinearTape(x2, w2, xs, ws, cfg)
     own = err is None
     if own:
@@ -225,7 +247,7 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     wop = qw.rows if isinstance(qw, SquareBlockTensor) else qw
     for t in ((qw.rows, qw.t) if isinstance(qw, SquareBlockTensor) else (qw,)):
         _keep(main, t)
-    y = gemm(qx, wop, out_dtype)
+    y = gemm(qx, wop, out_dtype) if accumulate == "f32" else gemm_emulated(qx, wop, accumulate)
     if own:
         _finish(err)
     return y, LinearTape(qx, qw, xs, ws, cfg)
@@ -241,9 +263,14 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     if es != (tokens, out_dim):
         raise ValueError(f"E has shape {es}, expected {(tokens, out_dim)}")
     mode = "posthoc" if cfg.posthoc else "exact"
-    dense = lambda t: t.float() if isinstance(t, torch.Tensor) else dequantize(t).float()   # noqa: E731
+    if accumulate not in ("f32", "f64"):
+        raise ValueError(f"unknown accumulate precision {accumulate!r}")
+    f64 = accumulate == "f64"                         # float64 products (the reference's oracle mode)
+    wide = torch.float64 if f64 else torch.float32
+    dx_dtype = torch.float64 if f64 else dx_dtype
+    dense = lambda t: _dense64(t).to(wide)            # noqa: E731
     if cfg.backward_scheme == "identity":             # no backward quantization (linear_graph.py:286-288)
-        ef = e2.float()
+        ef = e2.to(wide)
         return GradPair(torch.matmul(ef, dense(tape.qW)).to(dx_dtype), torch.matmul(ef.t(), dense(tape.qX)))
     own = err is None
     if own:
@@ -268,10 +295,10 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     def product(qa, qb, a_dense, b_dense, out_dtype):
         """gemm_emulated(qa, qb): the NVFP4 GEMM when both operands are quantized, else
         fp32 of the (dequantized) operands; a_dense/b_dense give the dense [M,K]/[N,K]."""
-        if qa is not None and qb is not None:
+        if qa is not None and qb is not None and not f64:
             return gemm(qa, qb, out_dtype)
-        a = dequantize(qa).float() if qa is not None else a_dense()
-        b = dequantize(qb).float() if qb is not None else b_dense()
+        a = dense(qa) if qa is not None else a_dense()
+        b = dense(qb) if qb is not None else b_dense()
         return torch.matmul(a, b.t()).to(out_dtype)
 
     with torch.cuda.stream(side):
@@ -284,9 +311,9 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         else:
             qet = qxt = None
         if qet is None and qxt is None:
-            dw = torch.matmul(e2.float().t(), dense(tape.qX))
+            dw = torch.matmul(e2.to(wide).t(), dense(tape.qX))
         else:
-            dw = product(qet, qxt, lambda: e2.float().t(), lambda: dense(tape.qX).t(), torch.float32)
+            dw = product(qet, qxt, lambda: e2.to(wide).t(), lambda: dense(tape.qX).t(), wide)
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
     qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
     qe = qwt = None
@@ -300,9 +327,9 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         qe = quant(e2, PAIR_DX, 0, "rows", both) if q_e else None
         qwt = quant(qw, PAIR_DX, 1, "cols" if isinstance(qw, torch.Tensor) else "tape", both) if q_w else None
     if qe is None and qwt is None:
-        dx = torch.matmul(e2.float(), dense(tape.qW)).to(dx_dtype)
+        dx = torch.matmul(e2.to(wide), dense(tape.qW)).to(dx_dtype)
     else:
-        dx = product(qe, qwt, lambda: e2.float(), lambda: dense(tape.qW).t(), dx_dtype)
+        dx = product(qe, qwt, lambda: e2.to(wide), lambda: dense(tape.qW).t(), dx_dtype)
     main.wait_stream(side)
     _keep(main, dw)
     e2.record_stream(side)

@@ -248,3 +248,41 @@ def test_baseline_quantizer_errors(cuda):
         q2.rht_sr(torch.ones(32, 64, device="cuda"), q2.SeedPair(1, 2), 3, 4)
     z = q2.quantize_sr(torch.zeros(0, 64, device="cuda"), 1, 2)
     assert z.shape == (0, 64) and float(z.scale32) == 0.0
+
+
+@pytest.mark.parametrize("fwd,bwd,abl,reuse", [("rtn_1x16_46", "ms_eden", "full", False),
+                                               ("rtn_1x16", "sr_rht", "b", False),
+                                               ("rtn_16x16", "sr_rht", "full", True),
+                                               ("identity", "identity", "full", False)])
+def test_accumulate_f64(cuda, fwd, bwd, abl, reuse):
+    """accumulate="f64" (linear_graph.py:190-205): float64 products of the same quantized
+    operands; only the DGEMM summation order differs from the reference's."""
+    q2 = _q2()
+    import torch
+    x = make("normal", (256, 384), seed=1)
+    w = to_bf16((make("normal", (256, 384), seed=2) / 16).astype(np.float32))
+    e = to_bf16((1e-2 * make("normal", (256, 256), seed=3)).astype(np.float32))
+    cfg = q2.LayerConfig(fwd, bwd, ablation=abl, reuse_forward_weights=reuse)
+    y, tape = q2.forward(_dev(x), _dev(w), cfg, accumulate="f64")
+    g = q2.backward(tape, _dev(e), q2.SeedPair(7, 9), accumulate="f64")
+    ry, rtape = O.forward(x, w, accumulate="f64", forward_scheme=fwd)
+    rdx, rdw = O.backward(rtape, e, O.SeedPair(7, 9), accumulate="f64", backward_scheme=bwd,
+                          reuse_forward_weights=reuse, ablation=abl)
+    for got, ref in ((y, ry), (g.dX, rdx), (g.dW, rdw)):
+        assert got.dtype == torch.float64
+        got = got.cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-12
+
+
+def test_gemm_emulated_operands(cuda):
+    q2 = _q2()
+    a = _dev(make("normal", (128, 256), seed=4), bf16=False)
+    b = _dev(make("normal", (64, 256), seed=5), bf16=False)
+    qa = q2.quantize_rtn_46(a)
+    ref = O.gemm_emulated(O.quantize_rtn_46(a.cpu().numpy()), b.cpu().numpy())
+    got = q2.gemm_emulated(qa, b).double().cpu().numpy()          # NVFP4 x dense: FP32 product
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-6
+    with pytest.raises(ValueError, match="inner dimensions disagree"):
+        q2.gemm_emulated(qa, b[:, :128])
+    with pytest.raises(ValueError, match="unknown accumulate precision"):
+        q2.gemm_emulated(qa, qa, "f16")
