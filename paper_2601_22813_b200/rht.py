@@ -122,7 +122,9 @@ def _rotation_call(x, chunk: int, pre, post, scale: float):
 
 def hadamard_128(x):
     """Orthonormal Hadamard of length-128 vectors (rht.py:121-130), literal float64 on the GPU."""
-    last = x.shape[-1] if hasattr(x, "shape") and len(x.shape) else len(x)
+    if not hasattr(x, "shape"):
+        x = np.asarray(x, dtype=np.float64)
+    last = x.shape[-1] if len(x.shape) else 0
     if last != CHUNK:
         raise ValueError(f"hadamard_128 requires length {CHUNK}, got {last}")
     return _rotation_call(x, CHUNK, None, None, CHUNK ** -0.5)
