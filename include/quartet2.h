@@ -137,17 +137,36 @@ int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr, const uint
                      int64_t R, int64_t K, uint64_t seed_sr, uint64_t sr_stream,
                      const q2_nvfp4* out, uint32_t* err, void* stream);
 
-/* Both backward operands that read E, from ONE read of E, post-hoc schedule:
- *  out_rows = pass2(pass1(E))      rows of E along N  (dgrad operand, pair_dx)
- *  out_cols = pass2(pass1(E^T))    rows of E^T along T (wgrad operand, pair_dw)
- * (linear_graph.py:306 and :325 with the posthoc.py:74-125 quantizer).  E is
- * bf16 [T, N] (row stride ld), T % 128 == N % 128 == 0; two q2_msed_quant
- * passes (rows and columns source) with their own sign vectors and streams.
- * ws_rows / ws_cols: q2_msed_ws_bytes(T, N) / q2_msed_ws_bytes(N, T).          */
+/* Both backward operands that read E, from ONE read of E (tensor-core kernel):
+ *  out_rows = MS(E)    rows of E along N  (dgrad operand, pair_dx)   linear_graph.py:306
+ *  out_cols = MS(E^T)  rows of E^T along T (wgrad operand, pair_dw)  linear_graph.py:325
+ * with the ms_eden_quantize (ms_eden.py:116-153) semantics of `mode`
+ * (Q2_MSED_EXACT / Q2_MSED_POW2) or pass2(pass1(.)) (posthoc.py:74-125,
+ * Q2_MSED_POSTHOC).  E is bf16 [T, N] (row stride ld), T % 128 == N % 128 == 0.
+ * Each 128x128 tile of E is read once; its row chunks and column chunks are
+ * rotated by two tensor-core MMAs from the same shared-memory tile.
+ * ws: q2_msed_dual_ws_bytes(T, N).
+ * q2_msed_dual_posthoc: the same in post-hoc mode with the per-operand
+ * workspaces of q2_msed_quant (q2_msed_ws_bytes(T, N) and (N, T)).            */
+size_t q2_msed_dual_ws_bytes(int64_t T, int64_t N);
+int q2_msed_dual(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
+                 const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
+                 uint64_t sr_stream_rows, uint64_t sr_stream_cols, int mode, const q2_nvfp4* out_rows,
+                 const q2_nvfp4* out_cols, void* ws, uint32_t* err, void* stream);
 int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
                          const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
                          uint64_t sr_stream_rows, uint64_t sr_stream_cols, const q2_nvfp4* out_rows,
                          const q2_nvfp4* out_cols, void* ws_rows, void* ws_cols, uint32_t* err, void* stream);
+/* Engine selection for q2_msed_quant / q2_msed_dual (process-wide setting):
+ * 0 auto (tensor-core kernel for the one-read dual E source; the literal
+ * float64 kernels for single-operand sources, faster there today), 1 the
+ * tensor-core kernel wherever eligible (bf16 or tape sources, dims multiples
+ * of 128), 2 the literal float64 kernels everywhere.  Results are identical. */
+int q2_set_msed_engine(int engine);
+/* Counters of the tensor-core MS-EDEN path since load (host-synchronous):
+ * out[0] = 128-chunks quantized, out[1] = chunks whose certification failed and
+ * that were recomputed by the literal float64 path.  reset != 0 zeroes them.   */
+int q2_msed_stats(unsigned long long out[2], int reset);
 
 /* Stochastic-rounding baselines.
  *   q2_quant_sr: quantize_sr (quantizers.py:139-161; ncaps 1, cap0 6) and

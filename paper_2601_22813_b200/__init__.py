@@ -8,7 +8,7 @@ meanings, computed by hand-written sm_100a CUDA in ``libquartet2.so``.
 from .rht import CHUNK, SeedPair, derive_stream, hadamard_128, prng_signs, prng_uniform, rht_apply, rht_inverse, sign_mask
 from .quantizers import (GROUP, absmax, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4Tensor, check_errors, dequantize,
                          deserialize_nvfp4, quantize_rtn, quantize_rtn_46, serialize_nvfp4, set_error_mode)
-from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual_posthoc,
+from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual, msed_dual_posthoc, msed_stats, set_msed_engine,
                       pass1, pass2,
                       posthoc_quantize, CostReport, KernelCost, cost_model, cost_model_table)
 from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr, sr_operand
@@ -20,7 +20,7 @@ from . import formats  # noqa: F401  (formats.py mirror: encode_fp4_rtn, ..., de
 __all__ = [
     "CHUNK", "GROUP", "GUARDED_SCALE_CAP", "FP8_RTN_MARGIN", "SeedPair", "derive_stream", "prng_uniform",
     "sign_mask", "NVFP4Tensor", "quantize_rtn", "quantize_rtn_46", "dequantize", "check_errors",
-    "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual_posthoc", "pass1", "pass2", "posthoc_quantize",
+    "set_error_mode", "ms_eden_quantize", "ms_eden_estimate_pair", "msed", "msed_dual", "msed_dual_posthoc", "msed_stats", "set_msed_engine", "pass1", "pass2", "posthoc_quantize",
     "ErNvfp4Tensor", "Pass1Reductions", "LayerConfig", "LinearTape", "GradPair", "baseline_config", "forward",
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
     "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",

@@ -23,7 +23,7 @@ Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF, Q2_ERR_SR_
 EXPORTS = (
     "q2_sf_bytes", "q2_version", "q2_amax", "q2_quant_fwd_ws_bytes", "q2_quant_fwd",
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
-    "q2_msed_dual_posthoc", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
+    "q2_msed_dual_posthoc", "q2_msed_dual", "q2_msed_dual_ws_bytes", "q2_msed_stats", "q2_set_msed_engine", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
     "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant", "q2_quant_square_block", "q2_sr_quant_src", "q2_quant_fwd_amax",
     "q2_rht", "q2_formats", "q2_eden_factors",
 )
@@ -57,6 +57,10 @@ _SIGS = {
     "q2_posthoc_pass2": (_I, [_P, _P, _P, _I64, _I64, _U64, _U64, _TP, _P, _P]),
     "q2_msed_dual_posthoc": (_I, [_P, _I64, _I64, _I64, _U32x4, _U32x4, _D, _D, _U64, _U64, _U64, _TP, _TP, _P, _P,
                                   _P, _P]),
+    "q2_msed_dual": (_I, [_P, _I64, _I64, _I64, _U32x4, _U32x4, _D, _D, _U64, _U64, _U64, _I, _TP, _TP, _P, _P, _P]),
+    "q2_msed_dual_ws_bytes": (ctypes.c_size_t, [_I64, _I64]),
+    "q2_msed_stats": (_I, [_P, _I]),
+    "q2_set_msed_engine": (_I, [_I]),
     "q2_gemm_tn": (_I, [_TP, _TP, _P, _I, _I64, _I, _P]),
     "q2_quant_sr_ws_bytes": (ctypes.c_size_t, []),
     "q2_sr_quant_src": (_I, [_P, _I, _TP, _I, _I64, _I64, _I64, _I, _U32x4, _I, _D, _D, _D, _D, _D, _U64, _U64, _U64,

@@ -16,8 +16,10 @@
 //            reference's non-pow2 scale32 needs the absmax before any code.
 //   pow2     msed64<PMAX> (pseudo max), msed64<QUANT, pow2>.
 #include <cuda_fp16.h>
+#include <cstdio>
 #include "tc_common.cuh"
 #include "msed64.cuh"
+#include "msed_tc.cuh"
 
 namespace q2 {
 
@@ -138,6 +140,113 @@ static M64Args base_args(const M64Src& s, int64_t R, int64_t K, const uint32_t s
   return a;
 }
 
+
+// ------------------------------------------------ tensor-core MS-EDEN launches
+// Engine of q2_msed_quant for single-operand sources: 0 auto (tensor-core kernel for the
+// dual E source only, where it is fastest today; literal float64 kernels otherwise),
+// 1 tensor-core kernel wherever eligible, 2 literal float64 kernels everywhere.
+static int g_msed_engine = -1;
+static int msed_engine() {
+  if (g_msed_engine < 0) g_msed_engine = getenv("Q2_MSED_LITERAL") ? 2 : 0;
+  return g_msed_engine;
+}
+static bool tc_disabled() { return msed_engine() == 2; }
+
+template <int SRC, int MODE>
+static int launch_tc(const TcArgs& a, int pow2, cudaStream_t st) {
+  using LY = TcLayout<SRC == TC_TAPE>;
+  auto k = msed_tc_kernel<SRC, MODE>;
+  static int attr_dev = -1;                      // per-device opt-in
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::SMEM) != cudaSuccess) return Q2_ECUDA;
+    attr_dev = dev;
+  }
+  CUtensorMap tm;
+  bool ok;
+  if (SRC == TC_TAPE)
+    ok = make_map(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.tape_codes, (uint64_t)(a.N / 2), (uint64_t)a.T,
+                  (uint64_t)(a.N / 2), 64, 128, CU_TENSOR_MAP_SWIZZLE_NONE);
+  else
+    ok = make_map(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.x, (uint64_t)a.N, (uint64_t)a.T, (uint64_t)a.ld * 2, 64, 128);
+  if (!ok) return Q2_ECUDA;
+  const int ntiles = a.tiles_r * a.tiles_c;
+  if (launch_pdl(k, dim3(std::min(ntiles, num_sms())), dim3(TC_THREADS), LY::SMEM, st, tm, a, pow2) != cudaSuccess)
+    return Q2_ECUDA;
+  return Q2_OK;
+}
+
+template <int MODE>
+static int dispatch_tc(int src, const TcArgs& a, int pow2, cudaStream_t st) {
+  switch (src) {
+    case TC_ROWS: return launch_tc<TC_ROWS, MODE>(a, pow2, st);
+    case TC_COLS: return launch_tc<TC_COLS, MODE>(a, pow2, st);
+    case TC_DUAL: return launch_tc<TC_DUAL, MODE>(a, pow2, st);
+    case TC_TAPE: return launch_tc<TC_TAPE, MODE>(a, pow2, st);
+  }
+  return Q2_EINVAL;
+}
+
+static int tc_pass2(const TcOut& o, uint32_t* err, cudaStream_t st) {
+  const int64_t quads = o.R * (o.K / 64);
+  if (quads >= (1ll << 31)) return Q2_EINVAL;
+  if (launch_pdl(tc_pass2_kernel, dim3((unsigned)std::max<int64_t>(1, (quads + 255) / 256)), dim3(256), 0, st,
+                 (const uint16_t*)o.aw, (const unsigned long long*)o.red, (uint32_t)o.R, (uint32_t)o.K,
+                 FastDiv((uint32_t)(o.K / 64)), o.sf, o.scale32, err) != cudaSuccess)
+    return Q2_ECUDA;
+  return Q2_OK;
+}
+
+// Run the tensor-core MS-EDEN for source kind src (TC_ROWS / TC_COLS / TC_DUAL / TC_TAPE) over
+// E [T, N] (or the tape [T, N]); outputs a.o[0] (rows) / a.o[1] (cols) already filled in.
+static int tc_run(int src, TcArgs& a, int mode, cudaStream_t st) {
+  static const int dbg = getenv("Q2_TC_DBG") ? atoi(getenv("Q2_TC_DBG")) : 0;
+  a.dbg = dbg;
+  static unsigned long long* trace = nullptr;
+  if (getenv("Q2_TC_TRACE")) {
+    if (!trace) cudaMalloc(&trace, 32 * 16 * 8);
+    cudaMemsetAsync(trace, 0, 32 * 16 * 8, st);
+    a.trace = trace;
+  }
+  a.tiles_r = (int)(a.T / 128);
+  a.tiles_c = (int)(a.N / 128);
+  a.fc = FastDiv((uint32_t)a.tiles_c);
+  for (int o = 0; o < 2; ++o)
+    if ((src >> o) & 1)
+      if (cudaMemsetAsync(a.o[o].red, 0, 16, st) != cudaSuccess) return Q2_ECUDA;
+  int rc;
+  if (mode == Q2_MSED_POSTHOC) {
+    if ((rc = dispatch_tc<TC_POSTHOC>(src, a, 0, st))) return rc;
+  if (a.trace) {
+    unsigned long long h[32 * 16];
+    cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[0];
+    for (int i = 0; i < 32; ++i) {
+      fprintf(stderr, "tile %2d:", i);
+      for (int j = 0; j < 10; ++j) fprintf(stderr, " %7.2f", h[i * 16 + j] ? (h[i * 16 + j] - t0) / 1e3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
+    for (int o = 0; o < 2; ++o)
+      if ((src >> o) & 1)
+        if ((rc = tc_pass2(a.o[o], a.err, st))) return rc;
+    return Q2_OK;
+  }
+  if ((rc = dispatch_tc<TC_ABSMAX>(src, a, 0, st))) return rc;
+  return dispatch_tc<TC_QUANT>(src, a, mode == Q2_MSED_POW2 ? 1 : 0, st);
+}
+
+static void tc_fill_out(TcOut& o, const q2_nvfp4* out, const uint32_t sign[4], uint64_t seed_sr, uint64_t stream,
+                        void* red, void* aw) {
+  o.codes = out->codes; o.sf = out->sf; o.scale32 = out->scale32;
+  o.R = out->R; o.K = out->K;
+  for (int i = 0; i < 4; ++i) o.sign[i] = sign[i];
+  o.sr_head = prng_head(seed_sr, stream);
+  o.red = static_cast<unsigned long long*>(red);
+  o.aw = static_cast<uint16_t*>(aw);
+}
+
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 }  // namespace q2
@@ -160,6 +269,23 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
+  // tensor-core path: bf16 or tape sources with 128-multiple dims
+  const bool tc_ok = msed_engine() == 1 && R > 0 && K > 0 && R % 128 == 0 && K % 128 == 0 &&
+                     (src_kind == Q2_SRC_TAPE_COLS || dtype == Q2_BF16) && R / 128 < (1 << 16) && K / 128 < (1 << 16);
+  if (tc_ok) {
+    TcArgs ta{};
+    const int osel = src_kind == Q2_SRC_ROWS ? 0 : 1;
+    tc_fill_out(ta.o[osel], out, sign_mask, seed_sr, sr_stream, w, w + 256);
+    ta.s = s; ta.inv_sqrt = inv_sqrt_chunk; ta.err = err;
+    int kind;
+    if (src_kind == Q2_SRC_ROWS) { ta.x = static_cast<const uint16_t*>(x); ta.ld = ld; ta.T = R; ta.N = K; kind = TC_ROWS; }
+    else if (src_kind == Q2_SRC_COLS) { ta.x = static_cast<const uint16_t*>(x); ta.ld = ld; ta.T = K; ta.N = R; kind = TC_COLS; }
+    else {
+      ta.tape_codes = tape->codes; ta.tape_sf = tape->sf; ta.tape_scale32 = tape->scale32;
+      ta.T = K; ta.N = R; kind = TC_TAPE;
+    }
+    if ((int64_t)(ta.T / 128) * (ta.N / 128) < (1ll << 24)) return tc_run(kind, ta, mode, st);
+  }
   M64Args a = base_args(src, R, K, sign_mask, s, inv_sqrt_chunk);
   a.red = reinterpret_cast<unsigned long long*>(w);
   a.err = err;
@@ -252,18 +378,85 @@ extern "C" int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr,
   return Q2_OK;
 }
 
-// Both backward operands that read E: MS(E) along rows (dgrad, pair sign_rows /
-// sr_stream_rows) and MS(E^T) (wgrad, pair sign_cols / sr_stream_cols), post-hoc
-// schedule.  x is bf16 [T, N], T % 128 == N % 128 == 0.
+// Both backward operands that read E, from ONE read of E (tensor-core kernel,
+// TC_DUAL): MS(E) along rows (dgrad operand, pair sign_rows / sr_stream_rows)
+// and MS(E^T) (wgrad operand, pair sign_cols / sr_stream_cols), in any mode.
+// x is bf16 [T, N], T % 128 == N % 128 == 0.  ws: q2_msed_dual_ws_bytes(T, N).
+extern "C" int q2_set_msed_engine(int engine) {
+  if (engine < 0 || engine > 2) return Q2_EINVAL;
+  g_msed_engine = engine;
+  return Q2_OK;
+}
+
+// Chunk counters of the tensor-core MS-EDEN since load: out[0] chunks quantized,
+// out[1] chunks deferred to the literal float64 path.  reset != 0 zeroes them.
+extern "C" int q2_msed_stats(unsigned long long* out, int reset) {
+  unsigned long long h[2] = {0ull, 0ull};
+  if (cudaMemcpyFromSymbol(h, g_tc_stats, sizeof(h)) != cudaSuccess) return Q2_ECUDA;
+  if (out) { out[0] = h[0]; out[1] = h[1]; }
+  if (reset) {
+    const unsigned long long z[2] = {0ull, 0ull};
+    if (cudaMemcpyToSymbol(g_tc_stats, z, sizeof(z)) != cudaSuccess) return Q2_ECUDA;
+  }
+  return Q2_OK;
+}
+
+extern "C" size_t q2_msed_dual_ws_bytes(int64_t T, int64_t N) {
+  return 256 + 2 * align256((size_t)T * (N / 16) * 2);
+}
+
+extern "C" int q2_msed_dual(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
+                            const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
+                            uint64_t sr_stream_rows, uint64_t sr_stream_cols, int mode, const q2_nvfp4* out_rows,
+                            const q2_nvfp4* out_cols, void* ws, uint32_t* err, void* stream) {
+  if (!x || !ws || !out_rows || !out_cols || !sign_rows || !sign_cols || T <= 0 || N <= 0 || T % CHUNK || N % CHUNK)
+    return Q2_EINVAL;
+  if (mode != Q2_MSED_EXACT && mode != Q2_MSED_POW2 && mode != Q2_MSED_POSTHOC) return Q2_EINVAL;
+  if (out_rows->R != T || out_rows->K != N || out_cols->R != N || out_cols->K != T) return Q2_EINVAL;
+  if (ld < N || (reinterpret_cast<uintptr_t>(x) & 15u) || (ld * 2) % 16) return Q2_EINVAL;
+  if ((T / 128) * (N / 128) >= (1ll << 24)) return Q2_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char* w = static_cast<char*>(ws);
+  if (tc_disabled()) {
+    // the literal kernels run the two operands one after the other on the same workspace
+    int rc = q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_ROWS, T, N, ld, sign_rows, s, inv_sqrt_chunk, seed_sr,
+                           sr_stream_rows, mode, out_rows, w, err, stream);
+    if (rc) return rc;
+    return q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_COLS, N, T, ld, sign_cols, s, inv_sqrt_chunk, seed_sr,
+                         sr_stream_cols, mode, out_cols, w, err, stream);
+  }
+  TcArgs ta{};
+  const size_t awb = align256((size_t)T * (N / 16) * 2);
+  tc_fill_out(ta.o[0], out_rows, sign_rows, seed_sr, sr_stream_rows, w, w + 256);
+  tc_fill_out(ta.o[1], out_cols, sign_cols, seed_sr, sr_stream_cols, w + 64, w + 256 + awb);
+  ta.x = static_cast<const uint16_t*>(x); ta.ld = ld; ta.T = T; ta.N = N;
+  ta.s = s; ta.inv_sqrt = inv_sqrt_chunk; ta.err = err;
+  return tc_run(TC_DUAL, ta, mode, st);
+}
+
 extern "C" int q2_msed_dual_posthoc(const void* x, int64_t T, int64_t N, int64_t ld, const uint32_t sign_rows[4],
                                     const uint32_t sign_cols[4], double s, double inv_sqrt_chunk, uint64_t seed_sr,
                                     uint64_t sr_stream_rows, uint64_t sr_stream_cols, const q2_nvfp4* out_rows,
                                     const q2_nvfp4* out_cols, void* ws_rows, void* ws_cols, uint32_t* err,
                                     void* stream) {
-  if (!x || T % CHUNK || N % CHUNK) return Q2_EINVAL;
-  int rc = q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_ROWS, T, N, ld, sign_rows, s, inv_sqrt_chunk, seed_sr,
-                         sr_stream_rows, Q2_MSED_POSTHOC, out_rows, ws_rows, err, stream);
-  if (rc) return rc;
-  return q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_COLS, N, T, ld, sign_cols, s, inv_sqrt_chunk, seed_sr,
-                       sr_stream_cols, Q2_MSED_POSTHOC, out_cols, ws_cols, err, stream);
+  // workspaces sized q2_msed_ws_bytes(T, N) / (N, T): red + words of each operand
+  if (!x || !ws_rows || !ws_cols || !out_rows || !out_cols || T <= 0 || N <= 0 || T % CHUNK || N % CHUNK)
+    return Q2_EINVAL;
+  if (out_rows->R != T || out_rows->K != N || out_cols->R != N || out_cols->K != T) return Q2_EINVAL;
+  if (ld < N || (reinterpret_cast<uintptr_t>(x) & 15u) || (ld * 2) % 16) return Q2_EINVAL;
+  if (tc_disabled() || (T / 128) * (N / 128) >= (1ll << 24)) {
+    int rc = q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_ROWS, T, N, ld, sign_rows, s, inv_sqrt_chunk, seed_sr,
+                           sr_stream_rows, Q2_MSED_POSTHOC, out_rows, ws_rows, err, stream);
+    if (rc) return rc;
+    return q2_msed_quant(x, Q2_BF16, nullptr, Q2_SRC_COLS, N, T, ld, sign_cols, s, inv_sqrt_chunk, seed_sr,
+                         sr_stream_cols, Q2_MSED_POSTHOC, out_cols, ws_cols, err, stream);
+  }
+  TcArgs ta{};
+  char* wr = static_cast<char*>(ws_rows);
+  char* wc = static_cast<char*>(ws_cols);
+  tc_fill_out(ta.o[0], out_rows, sign_rows, seed_sr, sr_stream_rows, wr, wr + 256);
+  tc_fill_out(ta.o[1], out_cols, sign_cols, seed_sr, sr_stream_cols, wc, wc + 256);
+  ta.x = static_cast<const uint16_t*>(x); ta.ld = ld; ta.T = T; ta.N = N;
+  ta.s = s; ta.inv_sqrt = inv_sqrt_chunk; ta.err = err;
+  return tc_run(TC_DUAL, ta, Q2_MSED_POSTHOC, static_cast<cudaStream_t>(stream));
 }

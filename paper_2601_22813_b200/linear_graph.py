@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .ms_eden import msed
+from .ms_eden import msed, msed_dual
 from .quantizers import (NVFP4Tensor, _err_word, _finish, as_device_matrix, dequantize, quantize_rtn_46,
                          stream_handle)
 from .rht import CHUNK, SeedPair, derive_stream
@@ -301,16 +301,33 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         b = dense(qb) if qb is not None else b_dense()
         return torch.matmul(a, b.t()).to(out_dtype)
 
+    # MS-EDEN of E for both GEMMs from one read of E (tensor-core dual kernel) when E is a
+    # bf16 [tokens, out] with both dims multiples of 128; identical results to two msed calls
+    dual = (not sr_scheme and q_e and q_w and q_et and q_xt and e2.dtype == torch.bfloat16
+            and tokens % CHUNK == 0 and out_dim % CHUNK == 0)
+    if dual:
+        qe_d, qet_d = msed_dual(e2, seeds, derive_stream(PAIR_DX, 0), PAIR_DX, derive_stream(PAIR_DW, 0), PAIR_DW,
+                                6.0, mode, err)
+        e_done = torch.cuda.Event()
+        e_done.record(main)
     with torch.cuda.stream(side):
         # dW = Q(E^T) Q(X^T)^T, inner dimension = tokens (side stream)
-        if (q_et or q_xt) if sr_scheme else (q_et and q_xt):
+        if dual:
+            qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape", True)
+            side.wait_event(e_done)
+            qet = qet_d
+            dw = product(qet, qxt, None, None, wide)
+            _keep(side, qet_d)                           # made on the caller's stream, read here
+        elif (q_et or q_xt) if sr_scheme else (q_et and q_xt):
             both = q_et and q_xt
             qet = quant(e2, PAIR_DW, 0, "cols", both) if q_et else None
             qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape",
                         both) if q_xt else None
         else:
             qet = qxt = None
-        if qet is None and qxt is None:
+        if dual:
+            pass
+        elif qet is None and qxt is None:
             dw = torch.matmul(e2.to(wide).t(), dense(tape.qX))
         else:
             dw = product(qet, qxt, lambda: e2.to(wide).t(), lambda: dense(tape.qX).t(), wide)
@@ -322,6 +339,9 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         qe = (quantize_sr_46 if sr_46 else quantize_sr)(e2, seeds.sr, derive_stream(PAIR_DX, 0), _err=err) \
             if q_e else None
         qwt = tape.qW.t
+    elif dual:
+        qe = qe_d
+        qwt = quant(qw, PAIR_DX, 1, "cols" if isinstance(qw, torch.Tensor) else "tape", True)
     elif (q_e or q_w) if sr_scheme else (q_e and q_w):
         both = q_e and q_w
         qe = quant(e2, PAIR_DX, 0, "rows", both) if q_e else None

@@ -87,35 +87,55 @@ def msed(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None, mode: 
     return out
 
 
-def msed_dual_posthoc(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: int, rot_cols: int, s=6.0,
-                      err=None):
-    """(posthoc MS(E), posthoc MS(E^T)) from one read of a bf16 E [T, N] (tensor-core rotations).
-
-    Equals (pass2(pass1(E)), pass2(pass1(E^T))) with the given tensor / rotation ids.
-    """
+def msed_dual(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: int, rot_cols: int, s=6.0,
+              mode: str = "exact", err=None):
+    """(MS(E), MS(E^T)) from ONE read of a bf16 E [T, N]: the dgrad and wgrad operands
+    that read E (linear_graph.py:306, :325), each equal to ``msed`` with its own tensor /
+    rotation ids.  Every 128x128 tile of E is rotated along its rows and its columns by
+    two tensor-core MMAs from the same shared-memory copy (q2_msed_dual)."""
     s = _grid_s(s)
     e2, shape, dt = as_device_matrix(e, "E")
     T, N = e2.shape
     if dt != _lib.Q2_BF16 or T % CHUNK or N % CHUNK:
-        raise ValueError("msed_dual_posthoc needs a bfloat16 E with both dims multiples of 128")
+        raise ValueError("msed_dual needs a bfloat16 E with both dims multiples of 128")
     L = _lib.lib()
     dev = e2.device
     qr, qc = NVFP4Tensor.empty((T, N), dev), NVFP4Tensor.empty((N, T), dev)
-    wr = torch.empty(L.q2_msed_ws_bytes(T, N), dtype=torch.uint8, device=dev)
-    wc = torch.empty(L.q2_msed_ws_bytes(N, T), dtype=torch.uint8, device=dev)
+    ws = torch.empty(L.q2_msed_dual_ws_bytes(T, N), dtype=torch.uint8, device=dev)
     own = err is None
     if own:
         err = _err_word(dev)
     a, b = qr.c(), qc.c()
-    rc = L.q2_msed_dual_posthoc(e2.data_ptr(), T, N, N, _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_rows))),
-                                _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_cols))), s, INV_SQRT_CHUNK,
-                                int(seeds.sr) & (2**64 - 1), sr_stream(int(id_rows)), sr_stream(int(id_cols)),
-                                ctypes.byref(a), ctypes.byref(b), wr.data_ptr(), wc.data_ptr(), err.data_ptr(),
-                                stream_handle())
-    _lib.check(rc, "msed_dual_posthoc")
+    rc = L.q2_msed_dual(e2.data_ptr(), T, N, e2.stride(0), _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_rows))),
+                        _lib._U32x4(*sign_mask(int(seeds.rht), int(rot_cols))), s, INV_SQRT_CHUNK,
+                        int(seeds.sr) & (2**64 - 1), sr_stream(int(id_rows)), sr_stream(int(id_cols)), _MODES[mode],
+                        ctypes.byref(a), ctypes.byref(b), ws.data_ptr(), err.data_ptr(), stream_handle())
+    _lib.check(rc, "msed_dual")
     if own:
         _finish(err)
     return qr, qc
+
+
+def msed_dual_posthoc(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: int, rot_cols: int, s=6.0,
+                      err=None):
+    """``msed_dual`` in post-hoc mode: (pass2(pass1(E)), pass2(pass1(E^T)))."""
+    return msed_dual(e, seeds, id_rows, rot_rows, id_cols, rot_cols, s, "posthoc", err)
+
+
+def set_msed_engine(engine: str) -> None:
+    """``"auto"`` (tensor-core kernel for the dual E source), ``"tc"`` (tensor-core kernel
+    wherever eligible) or ``"literal"`` (literal float64 kernels).  Results are identical."""
+    code = {"auto": 0, "tc": 1, "literal": 2}[engine]
+    _lib.check(_lib.lib().q2_set_msed_engine(code), "q2_set_msed_engine")
+
+
+def msed_stats(reset: bool = False):
+    """(chunks quantized, chunks recomputed by the literal float64 path) of the
+    tensor-core MS-EDEN kernels since load (host-synchronous)."""
+    out = (ctypes.c_ulonglong * 2)()
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().q2_msed_stats(out, int(reset)), "q2_msed_stats")
+    return int(out[0]), int(out[1])
 
 
 def ms_eden_quantize(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None,
