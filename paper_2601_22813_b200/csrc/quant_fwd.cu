@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) amax_kernel(const void* __restrict__ x, i
 // fast path and the reference semantics): exact threshold codes, sequential
 // float64 error, strict-less 4/6 selection.
 template <int DT>
-__device__ __forceinline__ uint3 quant_group_exact(const void* x, int64_t off, float scale32, int ncaps, double cap0,
+__device__ __noinline__ uint3 quant_group_exact(const void* x, int64_t off, float scale32, int ncaps, double cap0,
                                                 double cap1, uint32_t* err) {
   float v[16], gmax = 0.f;
   load_vec8(x, DT, off, v);
@@ -260,7 +260,9 @@ __device__ __forceinline__ void run_branch(const uint64_t (&vv)[8], const Branch
 // |S - S*| bound: q has relative error <= 2^-18 (bracket + rcp.approx + rz), so
 // by Cauchy-Schwarz sum 2|e|d <= 2^-17 sqrt(S Q); FFMA accumulation adds 2^-20 S.
 __device__ __forceinline__ float s_bound(float S, float Q) {
-  return 0x1p-17f * 1.01f * sqrtf(S * Q) + 0x1p-35f * Q + 0x1p-20f * S;
+  float r;                                          // sqrt.approx: relative error < 2^-22, covered by the 1.01
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(S * Q));
+  return 0x1p-17f * 1.01f * r + 0x1p-35f * Q + 0x1p-20f * S;
 }
 
 // ----- fix-up pass: the same certified decision with exact tie/midpoint resolution -----
@@ -419,19 +421,23 @@ __device__ __forceinline__ QuantConst quant_const(float scale32, int ncaps, doub
 
 // Persistent quantizer: a producer warp streams units of QT contiguous
 // 16-groups into a QNST-deep shared-memory ring with cp.async.bulk (TMA
-// engine); QT consumer threads quantize one group each per unit.  Fast path:
-// certified fp32 decisions (interval-checked E2M1 codes, bounded 4/6 error
-// comparison); uncertain groups run quant_group_exact.
+// engine); QT consumer threads quantize one group each per unit.  Every
+// decision is settled inside the kernel: the certified fp32 path decides
+// exact E2M1 ties and E4M3 midpoints exactly (FMA residual against t*E*scale32,
+// run_branch_t<true>), and the few groups it still cannot certify run the
+// literal float64 restatement in the same thread (quant_group_exact).  No
+// fix-up lists, no atomics, one pass.  Units run in reverse order so the tail
+// the amax pass read last is still in L2 when the quantize pass starts.
 #ifndef Q2_QMINB
 #define Q2_QMINB 2
 #endif
-constexpr int QT = 256, QNST = 4;
+constexpr int QT = 256, QNST = 8;
 
 template <int DT>
 __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
     const void* __restrict__ x, int64_t R, int64_t K, int ncaps, double cap0, double cap1, double scale_div,
     FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
-    float* __restrict__ scale32_out, uint32_t* __restrict__ fix_count, uint32_t* __restrict__ fix_list) {
+    float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
   constexpr int GB = DT == Q2_BF16 ? 32 : 64;               // bytes per 16-group
   extern __shared__ __align__(128) unsigned char qsm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(qsm + QNST * QT * GB);
@@ -449,9 +455,10 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
   if (warp == QT / 32) {                                      // producer warp
     if ((threadIdx.x & 31) == 0) {
       int i = 0;
-      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+      for (int64_t v = blockIdx.x; v < nunits; v += gridDim.x, ++i) {
+        const int64_t u = nunits - 1 - v;
         const int s = i % QNST;
-        if (i >= QNST) mbar_wait(empty0 + 8 * s, ((i / QNST) - 1) & 1);
+        if (i >= QNST) mbar_wait_sleep(empty0 + 8 * s, ((i / QNST) - 1) & 1);
         const uint32_t bytes = (uint32_t)((total - u * QT < QT ? total - u * QT : QT) * GB);
         mbar_expect_tx(full0 + 8 * s, bytes);
         bulk_load(smem_u32(qsm + s * QT * GB), static_cast<const char*>(x) + u * QT * GB, bytes, full0 + 8 * s);
@@ -462,18 +469,16 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
   const float amax = __uint_as_float(*amax_bits);
   const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
   if (blockIdx.x == 0 && threadIdx.x == 0) *scale32_out = scale32;
-  const double s32 = (double)scale32;
-  const double D0 = __dmul_rn(s32, cap0), D1 = __dmul_rn(s32, cap1);
-  const float invD0 = (float)(1.0 / D0), invD1 = (float)(1.0 / D1);
-  const float s32f = scale32;
-  const bool fast_ok = scale32 >= 0x1p-100f;                  // every d and 1/d stays normal in fp32
+  bool fast_ok;
+  const QuantConst qc = quant_const(scale32, ncaps, cap0, cap1, fast_ok);
   float* mids = reinterpret_cast<float*>(qsm + QNST * QT * GB + 128);
   if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
   asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
   int i = 0;
-  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
+  for (int64_t v = blockIdx.x; v < nunits; v += gridDim.x, ++i) {
+    const int64_t u = nunits - 1 - v;
     const int s = i % QNST;
-    mbar_wait(full0 + 8 * s, (i / QNST) & 1);
+    mbar_wait_sleep(full0 + 8 * s, (i / QNST) & 1);
     const int64_t gid = u * QT + threadIdx.x;
     const bool live = gid < total;
     uint32_t w[16];
@@ -488,114 +493,23 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(empty0 + 8 * s);  // slot may be refilled
     if (!live) continue;
-    const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+    uint32_t lo = 0, hi = 0, s8 = 0;
     uint64_t vv[8];
-    float gmax;
-    uint64_t vacc = 0;
-    if (DT == Q2_BF16) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t t = w[k] & 0x7FFF7FFFu;
-        asm("max.u16x2 %0, %0, %1;" : "+r"(m) : "r"(t));
-        vv[k] = pack2(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
-      }
-      gmax = __uint_as_float(max(m & 0xFFFFu, m >> 16) << 16);
-    } else {
-      uint32_t m = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        m = max(m, max(w[2 * k] & 0x7FFFFFFFu, w[2 * k + 1] & 0x7FFFFFFFu));
-        vv[k] = pack2(__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1]));
-      }
-      gmax = __uint_as_float(m);
-    }
-    uint32_t lo = 0, hi = 0, s8 = 0;
-    bool exact = !fast_ok;
-    if (amax == 0.f) {
-      exact = false;                                          // quantizers.py:219-220
-    } else if (gmax == 0.f && fast_ok) {
-      // all-zero group: codes 0 (q = +0 since d = 0), scale 0, both errors 0
-    } else if (!exact) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(vacc) : "l"(vv[k]));
-      const float V = hsum2(vacc);
-      const BranchConst c0 = branch_const(gmax, invD0, s32f, mids);
-      bool unc = c0.bad;
-      float S0;
-      uint32_t lo0, hi0;
-      run_branch(vv, c0, lo0, hi0, unc, S0);
-      if (ncaps == 1) {
-        exact = unc;
-        lo = lo0; hi = hi0; s8 = c0.s8;
-      } else {
-        const BranchConst c1 = branch_const(gmax, invD1, s32f, mids);
-        unc |= c1.bad;
-        float S1;
-        uint32_t lo1, hi1;
-        run_branch(vv, c1, lo1, hi1, unc, S1);
-        const float Q0 = V * c0.inv * c0.inv * 1.001f, Q1 = V * c1.inv * c1.inv * 1.001f;
-        const float E0 = c0.E * c0.E, E1 = c1.E * c1.E;
-        const float A0 = E0 * S0, A1 = E1 * S1;
-        const float M = E0 * s_bound(S0, Q0) + E1 * s_bound(S1, Q1) + 0x1p-22f * (A0 + A1);
-        const bool pick1 = A1 + M < A0, pick0 = A0 + M < A1;  // strict: ties keep caps[0]
-        exact = unc || !(pick0 || pick1);
-        lo = pick1 ? lo1 : lo0; hi = pick1 ? hi1 : hi0; s8 = pick1 ? c1.s8 : c0.s8;
-      }
-    }
-    if (exact) fix_list[atomicAdd(fix_count, 1u)] = (uint32_t)gid;   // resolved by quant_fix_kernel
-    *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
-    sf_store(sf, r, j, kpr, (uint8_t)s8);
-  }
-}
-
-// Exact float64 resolution of the groups the fast path could not certify.
-template <int DT>
-__global__ void __launch_bounds__(128) quant_fix_kernel(const void* __restrict__ x, int64_t K, int ncaps, double cap0,
-                                                        double cap1, double scale_div, FastDiv fgpr,
-                                                        const uint32_t* __restrict__ amax_bits,
-                                                        const uint32_t* __restrict__ fix_count,
-                                                        const uint32_t* __restrict__ fix_list, uint8_t* __restrict__ codes,
-                                                        uint8_t* __restrict__ sf, uint32_t* __restrict__ err) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float mids[128];
-  for (int t = threadIdx.x; t < 127; t += blockDim.x)
-    mids[t] = t < 126 ? 0.5f * (e4m3_valf(t) + e4m3_valf(t + 1)) : __int_as_float(0x7f800000);
-  __syncthreads();
-  const uint32_t n = *fix_count;
-  const float amax = __uint_as_float(*amax_bits);
-  const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
-  bool fast_ok;
-  const QuantConst qc = quant_const(scale32, ncaps, cap0, cap1, fast_ok);
-  const int64_t gpr = K / GROUP, kpr = sf_kblocks(K);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t gid = fix_list[i];
-    const uint32_t r = fgpr.div(gid), j = gid - r * (uint32_t)gpr;
-    uint32_t lo = 0, hi = 0, s8 = 0;
-    bool ok = false;
-    if (fast_ok) {
-      // most fix-ups are exact E2M1 ties or E4M3 midpoints: the fp32 path resolves them exactly
-      uint32_t w[16];
-      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(x) + (int64_t)gid * GROUP * (DT == Q2_BF16 ? 2 : 4));
-#pragma unroll
-      for (int q = 0; q < (DT == Q2_BF16 ? 2 : 4); ++q) {
-        const uint4 t = __ldg(src + q);
-        w[4 * q] = t.x; w[4 * q + 1] = t.y; w[4 * q + 2] = t.z; w[4 * q + 3] = t.w;
-      }
-      uint64_t vv[8];
-      const float gmax = unpack_group<DT>(w, vv);
-      auto elem = [&](int k) {
-        return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + (int64_t)gid * GROUP + k))
-                             : __ldg(static_cast<const float*>(x) + (int64_t)gid * GROUP + k);
+    const float gmax = unpack_group<DT>(w, vv);
+    // an all-zero group (or tensor, quantizers.py:219-220): codes 0, scale 0, both errors 0
+    if (amax != 0.f && !(gmax == 0.f && fast_ok)) {
+      auto elem = [&](int k) {            // the (rare) tie test re-reads element k
+        return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + gid * GROUP + k))
+                             : __ldg(static_cast<const float*>(x) + gid * GROUP + k);
       };
-      ok = gmax > 0.f && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8);
+      const bool ok = fast_ok && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8);
+      if (!ok) {                                              // the literal float64 restatement
+        const uint3 e = quant_group_exact<DT>(x, gid * GROUP, scale32, ncaps, cap0, cap1, err);
+        lo = e.x; hi = e.y; s8 = e.z;
+      }
     }
-    if (!ok) {                                                // the literal float64 restatement
-      const uint3 e = quant_group_exact<DT>(x, (int64_t)gid * GROUP, scale32, ncaps, cap0, cap1, err);
-      lo = e.x; hi = e.y; s8 = e.z;
-    }
-    *reinterpret_cast<uint2*>(codes + (int64_t)gid * 8) = make_uint2(lo, hi);
+    const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+    *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
     sf_store(sf, r, j, kpr, (uint8_t)s8);
   }
 }
@@ -627,26 +541,36 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
   return Q2_OK;
 }
 
-// ws: [0] amax bits, [1] fix-up count, [4..] fix-up list (one u32 per group).
+// ws: [0] amax bits (16 bytes; the size formula keeps its old, larger value for ABI stability).
 extern "C" size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K) { return 16 + 4 * (size_t)R * (size_t)(K / 16); }
+
+// cudaFuncSetAttribute applies to the current device only: opt in once per device.
+template <class F>
+static bool smem_opt_in(F* fn, int bytes, unsigned& done_mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return false;
+  if (done_mask & (1u << dev)) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  done_mask |= 1u << dev;
+  return true;
+}
 
 static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0,
                      double cap1, double scale_div, const q2_nvfp4* out, const uint32_t* amax_in, void* ws,
                      uint32_t* err, void* stream) {
   if (!out || !ws || (ncaps != 1 && ncaps != 2) || out->R != R || out->K != K) return Q2_EINVAL;
+  if (R < 0 || K < 0 || K % 16 || (dtype != Q2_BF16 && dtype != Q2_F32)) return Q2_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (R == 0 || K == 0)                                   // empty tensor: the zero tensor (quantizers.py:219-220)
     return cudaMemsetAsync(out->scale32, 0, 4, s) == cudaSuccess ? Q2_OK : Q2_ECUDA;
-  uint32_t* amax_ws = static_cast<uint32_t*>(ws);
-  uint32_t* fix_count = amax_ws + 1;
-  uint32_t* fix_list = amax_ws + 4;
-  if (cudaMemsetAsync(amax_ws, 0, 8, s) != cudaSuccess) return Q2_ECUDA;
-  int rc = amax_in ? Q2_OK : q2_amax(x, dtype, R, K, ld, amax_ws, err, stream);
-  if (rc) return rc;
-  const uint32_t* amax = amax_in ? amax_in : amax_ws;
+  if (!x) return Q2_EINVAL;
+  // every argument check happens before the first launch: Q2_EINVAL means nothing was launched.
   // The quantize pass streams contiguous rows (the host wrapper makes views contiguous).
-  if (ld != K || (reinterpret_cast<uintptr_t>(x) & 15u) || K / 16 >= (1ll << 31) || R * (K / 16) >= (1ll << 31))
+  if (ld != K || (reinterpret_cast<uintptr_t>(x) & 31u) || K / 16 >= (1ll << 31) || R * (K / 16) >= (1ll << 31))
     return Q2_EINVAL;
+  const int esz = dtype == Q2_BF16 ? 2 : 4;
+  if ((ld * esz) % 32) return Q2_EINVAL;
+  uint32_t* amax_ws = static_cast<uint32_t*>(ws);
   const int64_t groups = R * (K / 16);
   const int64_t units = (groups + QT - 1) / QT;
   int dev = 0, nsm = 148;
@@ -654,25 +578,25 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, Q2_QMINB * nsm));
   const FastDiv fg((uint32_t)(K / 16));
-  if (dtype == Q2_BF16) {
-    const int smem = QNST * QT * 32 + 128 + 512;
-    static bool a0 = false;
-    if (!a0) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a0 = true; }
-    launch_pdl(quant_fwd_kernel<Q2_BF16>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
-                                                             out->codes, out->sf, out->scale32, fix_count, fix_list);
-    launch_pdl(quant_fix_kernel<Q2_BF16>, dim3(8 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
-                                                      fix_list, out->codes, out->sf, err);
-  } else {
-    const int smem = QNST * QT * 64 + 128 + 512;
-    static bool a1 = false;
-    if (!a1) { cudaFuncSetAttribute(quant_fwd_kernel<Q2_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); a1 = true; }
-    launch_pdl(quant_fwd_kernel<Q2_F32>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1, scale_div, fg, amax,
-                                                            out->codes, out->sf, out->scale32, fix_count, fix_list);
-    launch_pdl(quant_fix_kernel<Q2_F32>, dim3(8 * nsm), dim3(128), 0, s, x, K, ncaps, cap0, cap1, scale_div, fg, amax, fix_count,
-                                                     fix_list, out->codes, out->sf, err);
+  const int smem = QNST * QT * (dtype == Q2_BF16 ? 32 : 64) + 128 + 512;
+  static unsigned attr_bf16 = 0, attr_f32 = 0;
+  if (!(dtype == Q2_BF16 ? smem_opt_in(quant_fwd_kernel<Q2_BF16>, smem, attr_bf16)
+                         : smem_opt_in(quant_fwd_kernel<Q2_F32>, smem, attr_f32)))
+    return Q2_ECUDA;
+  if (!amax_in) {
+    if (cudaMemsetAsync(amax_ws, 0, 4, s) != cudaSuccess) return Q2_ECUDA;
+    const int rc = q2_amax(x, dtype, R, K, ld, amax_ws, err, stream);
+    if (rc) return rc;
   }
-  Q2_CHECK_LAUNCH();
-  return Q2_OK;
+  const uint32_t* amax = amax_in ? amax_in : amax_ws;
+  cudaError_t e;
+  if (dtype == Q2_BF16)
+    e = launch_pdl(quant_fwd_kernel<Q2_BF16>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1,
+                   scale_div, fg, amax, out->codes, out->sf, out->scale32, err);
+  else
+    e = launch_pdl(quant_fwd_kernel<Q2_F32>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1,
+                   scale_div, fg, amax, out->codes, out->sf, out->scale32, err);
+  return e == cudaSuccess ? Q2_OK : Q2_ECUDA;
 }
 
 extern "C" int q2_quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps,

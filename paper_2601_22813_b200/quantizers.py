@@ -176,8 +176,10 @@ def as_device_matrix(x, what: str = "input"):
     if len(shape) == 0:
         raise ValueError(f"{what}: expected at least one dimension")
     x2 = x.reshape(-1, shape[-1]) if len(shape) != 2 else x
-    if not x2.is_contiguous() or x2.data_ptr() % 16:
+    if not x2.is_contiguous():
         x2 = x2.contiguous()
+    if x2.data_ptr() % 32:                  # the vector loads need 32-byte aligned rows (offset views)
+        x2 = x2.clone()
     return x2, shape, (_lib.Q2_BF16 if x.dtype == torch.bfloat16 else _lib.Q2_F32)
 
 

@@ -1,5 +1,5 @@
-"""Forward-quantizer breakdown at the bench shapes: amax / quantize / fix-up
-kernel times (CUDA events, L2 flushed) and the fix-up list length.
+"""Forward-quantizer timing at the bench shapes: amax + quantize pass vs the amax
+pass alone (CUDA events, L2 flushed).
 
     python tools/quant_probe.py
 """
@@ -45,9 +45,9 @@ def main():
                 torch.cuda.synchronize()
                 tot += s.elapsed_time(e)
             us = tot / 20 * 1e3
-            gb = R * K * (4 if lab.startswith("quant") else 2) / us / 1e3
-            print(f"{name:16s} {lab:16s} {us:8.1f} us  {gb:7.0f} GB/s (2 reads)" if lab.startswith("quant")
-                  else f"{name:16s} {lab:16s} {us:8.1f} us  {gb:7.0f} GB/s")
+            gb = R * K * (2.5625 if lab.startswith("quant") else 2) / us / 1e3
+            print(f"{name:16s} {lab:16s} {us:8.1f} us  {gb:7.0f} GB/s credited (2.5625 B/elem, amax incl.)"
+                  if lab.startswith("quant") else f"{name:16s} {lab:16s} {us:8.1f} us  {gb:7.0f} GB/s")
 
 
 if __name__ == "__main__":
