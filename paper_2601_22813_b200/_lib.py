@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libquartet2.so")
+LIB_PATH = os.environ.get("Q2_LIB_OVERRIDE") or os.path.join(_HERE, "libquartet2.so")   # override: A/B timing tools only
 
 Q2_OK, Q2_EINVAL, Q2_ECUDA = 0, 1, 2
 Q2_BF16, Q2_F32, Q2_F64 = 0, 1, 2

@@ -203,12 +203,6 @@ static int tc_pass2(const TcOut& o, uint32_t* err, cudaStream_t st) {
 static int tc_run(int src, TcArgs& a, int mode, cudaStream_t st) {
   static const int dbg = getenv("Q2_TC_DBG") ? atoi(getenv("Q2_TC_DBG")) : 0;
   a.dbg = dbg;
-  static unsigned long long* trace = nullptr;
-  if (getenv("Q2_TC_TRACE")) {
-    if (!trace) cudaMalloc(&trace, 32 * 16 * 8);
-    cudaMemsetAsync(trace, 0, 32 * 16 * 8, st);
-    a.trace = trace;
-  }
   a.tiles_r = (int)(a.T / 128);
   a.tiles_c = (int)(a.N / 128);
   a.fc = FastDiv((uint32_t)a.tiles_c);
@@ -218,16 +212,6 @@ static int tc_run(int src, TcArgs& a, int mode, cudaStream_t st) {
   int rc;
   if (mode == Q2_MSED_POSTHOC) {
     if ((rc = dispatch_tc<TC_POSTHOC>(src, a, 0, st))) return rc;
-  if (a.trace) {
-    unsigned long long h[32 * 16];
-    cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[0];
-    for (int i = 0; i < 32; ++i) {
-      fprintf(stderr, "tile %2d:", i);
-      for (int j = 0; j < 10; ++j) fprintf(stderr, " %7.2f", h[i * 16 + j] ? (h[i * 16 + j] - t0) / 1e3 : -1.0);
-      fprintf(stderr, "\n");
-    }
-  }
     for (int o = 0; o < 2; ++o)
       if ((src >> o) & 1)
         if ((rc = tc_pass2(a.o[o], a.err, st))) return rc;

@@ -184,7 +184,7 @@ template <int SRC, int DT, int MODE>
 __global__ void __launch_bounds__(M64_THREADS, 1) msed64_kernel(const __grid_constant__ CUtensorMap tm, M64Args a) {
   using TL = M64Tile<SRC, DT>;
   extern __shared__ __align__(1024) unsigned char m64_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(m64_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* smem = m64_raw + ((1024u - (smem_u32(m64_raw) & 1023u)) & 1023u);   // stays a shared-space pointer (LDS/STS, not generic LD/ST)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TL::OFF_BAR);
   const uint32_t bar_full = smem_u32(bars), bar_empty = smem_u32(bars + TL::STAGES);
   // tape: decoded tile b complete (every warp decoded its part) / consumed (every warp loaded it)

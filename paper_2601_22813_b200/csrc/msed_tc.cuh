@@ -52,7 +52,7 @@ namespace q2 {
 enum { TC_ABSMAX = 0, TC_QUANT = 1, TC_POSTHOC = 2 };
 enum { TC_ROWS = 1, TC_COLS = 2, TC_DUAL = 3, TC_TAPE = 6 };   // bit 0 rows, bit 1 cols, bit 2 tape
 
-constexpr int TC_THREADS = 448;
+constexpr int TC_THREADS = 704;                  // 6 + 16 epilogue warps
 constexpr int TC_TILE = 32768;                   // 128 x 128 bf16
 constexpr int TC_RAW = 10240;                    // tape raw tile: codes 8 KB + scales 2 KB
 constexpr int TC_NRAW = 3;
@@ -60,19 +60,20 @@ constexpr int TC_META = 4;                       // metadata ring (tile flags)
 constexpr int TC_META_BYTES = 16;
 constexpr int TC_DEF_CAP = 256;
 constexpr int TC_PF = 6;                         // tiles prefetched into L2 ahead of the TMA ring
-// Shared memory: H half (16 KB) | NS stages of main + small (64 KB each) | tape raw ring |
+// Shared memory: B operands diag(s) H per orientation (32 KB each) | NS stages of main + small (64 KB each) | tape raw ring |
 // metadata ring | deferred list | misc | barriers.  bf16 sources: 3 stages
 // (TMA writes the main buffer in place); tape: 2 stages + a 3-deep raw ring.
 template <bool TAPE>
 struct TcLayout {
-  static constexpr int NS = TAPE ? 2 : 3;
-  static constexpr int OFF_B = 0;
-  static constexpr int OFF_ST = 16384;
+  static constexpr int NS = 2;
+  static constexpr int OFF_B = 0;                  // [orientation] 128 x 128 bf16, K-major, 128B swizzle
+  static constexpr int OFF_ST = TAPE ? 32768 : 65536;
   static constexpr int OFF_RAW = OFF_ST + NS * 2 * TC_TILE;
   static constexpr int OFF_META = OFF_RAW + (TAPE ? TC_NRAW * TC_RAW : 0);
   static constexpr int OFF_DEF = OFF_META + TC_META * TC_META_BYTES;
   static constexpr int OFF_MISC = OFF_DEF + TC_DEF_CAP * 4;
-  static constexpr int OFF_BAR = OFF_MISC + 256;
+  static constexpr int OFF_XCH = OFF_MISC + 256;   // epilogue pair exchange: float4 [2][128][2] | u32 [2][128][2]
+  static constexpr int OFF_BAR = OFF_XCH + 8192 + 2048;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 static_assert(TcLayout<false>::SMEM <= 232448 && TcLayout<true>::SMEM <= 232448, "shared memory budget");
@@ -96,17 +97,7 @@ struct TcArgs {
   double s, inv_sqrt;
   uint32_t* err;
   int dbg;                                         // timing probes: 1 epilogue drains only, 2 + no split work
-  unsigned long long* trace;                       // optional per-tile timeline of CTA 0 (Q2_TC_TRACE)
 };
-__device__ __forceinline__ unsigned long long tc_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// trace slots per tile (CTA 0, first 32 tiles): 0 TMA issued, 1 split start, 2 split end, 3 MMA start,
-// 4 MMA issued, 5 WG0 meta, 6 WG0 tfull, 7 WG0 beta done, 8 WG0 groups done, 9 WG0 end
-#define TC_TR(slot) do { if (a.trace && blockIdx.x == 0 && it < 32) a.trace[it * 16 + (slot)] = tc_now(); } while (0)
-
 // chunks processed / deferred to the literal path since load (q2_msed_stats)
 __device__ unsigned long long g_tc_stats[2];
 
@@ -322,11 +313,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
                                                                  int pow2) {
   constexpr bool DUAL = SRC == TC_DUAL, TAPE = SRC == TC_TAPE;
   constexpr int ONLY = SRC == TC_ROWS ? 0 : 1;                // orientation of single-orientation sources
-  constexpr int NJ = DUAL ? 4 : 2;                            // jobs per tile
+  constexpr int NB = DUAL ? 2 : 1;                            // orientations (B operands, accumulators) per tile
   using LY = TcLayout<TAPE>;
   constexpr int NS = LY::NS;
   extern __shared__ __align__(1024) unsigned char tc_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* smem = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);   // stays a shared-space pointer (LDS/STS, not generic LD/ST)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LY::OFF_BAR);
   const uint32_t bar_full = smem_u32(bars);                   // [3] TMA landed (main stage / tape raw slot)
   const uint32_t bar_rawe = smem_u32(bars + 3);               // [3] tape raw slot decoded (4 warps)
@@ -352,24 +343,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(bar_tfull + 8 * b, 1);
-      mbar_init(bar_tempty + 8 * b, 4);
+      mbar_init(bar_tempty + 8 * b, 8);
       mbar_init(bar_mfull + 8 * b, 4);
-      mbar_init(bar_mempty + 8 * b, 8);
+      mbar_init(bar_mempty + 8 * b, 16);
     }
     for (int i = 0; i < 24; ++i) misc[i] = 0;
     mbar_fence_init();
   }
-  // H[k][j] for j < 64 (K-major B operand: row j, 2 slabs of 64 k), bf16 +-1
-  for (int i = threadIdx.x; i < 64 * 16; i += TC_THREADS) {
-    const int j = i >> 4, p = i & 15;
+  // B operands: B_o[j][k] = s_o[k] H[k][j] (the sign vector of orientation o folded into the
+  // Hadamard matrix), bf16 +-1, K-major rows j, two 64-k slabs of 16 KB, 128B swizzle
+  for (int i = threadIdx.x; i < NB * 128 * 16; i += TC_THREADS) {
+    const int bi = i >> 11, j = (i >> 4) & 127, p = i & 15;
+    const uint32_t* sg = a.o[DUAL ? bi : ONLY].sign;
     uint32_t w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int k0 = p * 8 + 2 * e;
-      const uint32_t h0 = (__popc(k0 & j) & 1) ? 0xBF80u : 0x3F80u, h1 = (__popc((k0 + 1) & j) & 1) ? 0xBF80u : 0x3F80u;
-      w[e] = h0 | (h1 << 16);
+      const int k0 = p * 8 + 2 * e, k1 = k0 + 1;
+      const uint32_t n0 = (__popc(k0 & j) + (sg[k0 >> 5] >> (k0 & 31))) & 1u;
+      const uint32_t n1 = (__popc(k1 & j) + (sg[k1 >> 5] >> (k1 & 31))) & 1u;
+      w[e] = (n0 ? 0xBF80u : 0x3F80u) | ((n1 ? 0xBF80u : 0x3F80u) << 16);
     }
-    *reinterpret_cast<uint4*>(smem + LY::OFF_B + (p >> 3) * 8192 + tc_sw(j, p & 7)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(smem + LY::OFF_B + bi * 32768 + (p >> 3) * 16384 + tc_sw(j, p & 7)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
@@ -416,7 +411,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int tr = (int)a.fc.div((uint32_t)t), tcl = t - tr * a.tiles_c;
         prefetch(t + TC_PF * gridDim.x);
-        TC_TR(0);
         if (!TAPE) {
           const int s = it % NS;
           if (it >= NS) mbar_wait_sleep(bar_sempty + 8 * s, ((it / NS) - 1) & 1);
@@ -440,28 +434,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
   } else if (warp == 1) {
     // ----------------------------------------------------------------- MMA
     if (lane == 0) {
-      const uint32_t idk = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
-      const uint32_t bb = smem_u32(smem + LY::OFF_B);
+      const uint32_t idk = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
       int it = 0;
-      uint64_t usebits = 0;                                  // per-buffer use counts mod 256 (bytes)
+      uint32_t ubuf0 = 0, ubuf1 = 0;                         // uses of the two accumulator buffers
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int s = it % NS;
-        mbar_wait(bar_split + 8 * s, (it / NS) & 1);
-        TC_TR(3);
+        mbar_wait_sleep(bar_split + 8 * s, (it / NS) & 1);
         tc_fence_after();
         const uint32_t flags = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + (it % TC_META) * TC_META_BYTES)[0];
         const bool has_small = flags & 1u;
         const uint32_t mainb = smem_u32(smem + LY::OFF_ST + s * 2 * TC_TILE), smallb = mainb + TC_TILE;
 #pragma unroll 1
-        for (int jj = 0; jj < NJ; ++jj) {
-          const int o = DUAL ? (jj & 1) : ONLY, h = DUAL ? (jj >> 1) : jj;
-          const int b = DUAL ? jj : 2 * (it & 1) + jj;
-          const int ub = (int)((usebits >> (8 * b)) & 0xFFu);
-          if (ub > 0) mbar_wait(bar_tempty + 8 * b, (ub - 1) & 1);
-          usebits += 1ull << (8 * b);
+        for (int jj = 0; jj < NB; ++jj) {
+          // accumulator buffer (256 columns: Y1 = H.main | Y2 = H.small, N = 128 each):
+          // dual: one per orientation; single orientation: alternating tiles
+          const int o = DUAL ? jj : ONLY, buf = DUAL ? jj : (it & 1);
+          const uint32_t ub = buf ? ubuf1 : ubuf0;
+          if (ub > 0) mbar_wait_sleep(bar_tempty + 8 * buf, (ub - 1) & 1);
+          if (buf) ++ubuf1; else ++ubuf0;
           tc_fence_after();
           const uint32_t id = idk | (o ? (1u << 15) : 0u);
-          const uint32_t d = tmem + 128 * b;
+          const uint32_t bb = smem_u32(smem + LY::OFF_B + jj * 32768);
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
             if (part == 1 && (!has_small || a.dbg == 3)) break;
@@ -471,35 +464,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             for (int kk = 0; kk < 8; ++kk) {
               const uint64_t ad = o == 0 ? desc_sw128(ab + (kk >> 2) * 16384 + (kk & 3) * 32)
                                          : desc_mn_sw128(ab + kk * 2048, 16384, 1024);
-              const uint64_t bd = desc_sw128(bb + (kk >> 2) * 8192 + (kk & 3) * 32);
-              tc_mma_f16(d + 64 * part, ad, bd, id | ((h && kk >= 4) ? (1u << 14) : 0u), kk > 0);
+              const uint64_t bd = desc_sw128(bb + (kk >> 2) * 16384 + (kk & 3) * 32);
+              tc_mma_f16(tmem + 256 * buf + 128 * part, ad, bd, id, kk > 0);
             }
           }
-          tc_commit(bar_tfull + 8 * b);
+          tc_commit(bar_tfull + 8 * buf);
         }
         tc_commit(bar_sempty + 8 * s);
-        TC_TR(4);
       }
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------- split
     const int sw = warp - 2, st = threadIdx.x - 64;          // split thread 0..127
     const int piece = st & 7;                                 // fixed 16-B column piece
-    // signs folded into x: x' = x * s_rows[n] * s_cols[t] (tape: the row sign at decode)
-    const uint32_t* sgn_n = a.o[0].sign;                      // rows orientation rotates along n
-    const uint32_t* sgn_t = a.o[1].sign;                      // cols orientation rotates along t
-    uint32_t csgn[2][4];
-#pragma unroll
-    for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int n0 = sl * 64 + piece * 8 + 2 * e;
-        const bool use_n = (SRC & 1) != 0;
-        const uint32_t b0 = use_n ? (sgn_n[n0 >> 5] >> (n0 & 31)) & 1u : 0u;
-        const uint32_t b1 = use_n ? (sgn_n[(n0 + 1) >> 5] >> ((n0 + 1) & 31)) & 1u : 0u;
-        csgn[sl][e] = (b0 << 15) | (b1 << 31);
-      }
-    const bool use_t = (SRC & 2) && !TAPE;
+    // (the rotation signs live in the B operands: the split only separates main / small)
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int s = it % NS, m = it % TC_META;
@@ -507,7 +485,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       unsigned char* smallp = mainp + TC_TILE;
       uint32_t* metau = reinterpret_cast<uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES);
       if (!TAPE) mbar_wait_sleep(bar_full + 8 * s, (it / NS) & 1);
-      if (st == 0) TC_TR(1);
       if (it >= TC_META) mbar_wait_sleep(bar_mempty + 8 * m, ((it / TC_META) - 1) & 1);
       if (TAPE) {
         // decode the NVFP4 tape tile: tape row kr = st, 128 tape columns; FP4 * E4M3 has
@@ -518,7 +495,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         const int tr = (int)a.fc.div((uint32_t)t);
         const unsigned char* raw = smem + LY::OFF_RAW + rs * TC_RAW;
         const int kr = st, L = kr & 31;
-        const uint32_t rsg = ((sgn_t[kr >> 5] >> (kr & 31)) & 1u) ? 0x80008000u : 0u;
 #pragma unroll 1
         for (int qd = 0; qd < 4; ++qd) {                       // 32 tape columns per quarter
           const uint4 cw = *reinterpret_cast<const uint4*>(raw + kr * 64 + qd * 16);
@@ -543,7 +519,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
                 : "=f"(f0), "=f"(f1) : "r"(pv));
             asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(ov[i]) : "f"(f1), "f"(f0));
-            ov[i] ^= rsg;
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -562,7 +537,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       }
       // pass 1: tile max of |x| (bf16 bits)
       uint32_t mx = 0;
-#pragma unroll 4
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int p = st + 128 * i, sl = p >> 10, row = (p & 1023) >> 3;
         const uint4 v = *reinterpret_cast<const uint4*>(mainp + sl * 16384 + tc_sw(row, piece));
@@ -585,12 +560,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const uint32_t thr2 = thr | (thr << 16);
       // pass 2: main/small split with the signs folded in
       uint32_t anys = 0;
-#pragma unroll 2
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int p = st + 128 * i, sl = p >> 10, row = (p & 1023) >> 3;
         const uint32_t off = sl * 16384 + tc_sw(row, piece);
         const uint4 v = *reinterpret_cast<const uint4*>(mainp + off);
-        const uint32_t rsg = use_t ? (((sgn_t[row >> 5] >> (row & 31)) & 1u) ? 0x80008000u : 0u) : 0u;
         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
         uint32_t mo[4], so[4];
 #pragma unroll
@@ -601,9 +575,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           const uint32_t tb = (w | 0x80008000u) - thr2;
           uint32_t mask;
           asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(mask) : "r"(tb));
-          const uint32_t sg = csgn[sl][e] ^ rsg;
-          mo[e] = (w & mask) ^ sg;
-          so[e] = (w & ~mask) ^ sg;
+          mo[e] = w & mask;
+          so[e] = w & ~mask;
           anys |= so[e];
         }
         *reinterpret_cast<uint4*>(mainp + off) = make_uint4(mo[0], mo[1], mo[2], mo[3]);
@@ -619,7 +592,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         if (nonfin) misc[12] |= 1u;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (st == 0) TC_TR(2);
       if (lane == 0) {
         mbar_arrive(bar_split + 8 * s);
         mbar_arrive(bar_mfull + 8 * m);
@@ -627,10 +599,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     }
   } else {
     // ----------------------------------------------------------- epilogue
-    // One thread per chunk (TMEM lane rt): two 64-output jobs of 4 groups each.
-    const int wg = warp >= 10 ? 1 : 0;
-    const int q = warp & 3, rt = 32 * q + lane;
-    const int o = DUAL ? wg : ONLY;
+    // 16 warps.  Warp e = warp - 6 reads TMEM lanes 32q..32q+31 (q = warp & 3; one lane =
+    // one chunk rt), slot = (e >> 2) & 1, half h = e >> 3.  The two threads (h = 0, 1) of a
+    // chunk take its groups 0-3 / 4-7 (the two 64-output jobs) and exchange the Y2 norm, the
+    // EDEN sums and the deferral flags through shared memory (pair barrier 2 + 4 slot + q).
+    // Dual: slot = orientation.  Single orientation: slot = tile parity.
+    const int e = warp - 6, q = warp & 3, slot = (e >> 2) & 1, h = e >> 3;
+    const int rt = 32 * q + lane;
+    const int o = DUAL ? slot : ONLY;
+    const uint32_t pbar = 2 + 4 * slot + q;
+    float4* const xch = reinterpret_cast<float4*>(smem + LY::OFF_XCH) + (slot * 128 + rt) * 2;      // [2]
+    uint32_t* const fl2 = reinterpret_cast<uint32_t*>(smem + LY::OFF_XCH + 8192) + (slot * 128 + rt) * 2;
     // per-thread constants of this thread's orientation (no dynamic indexing of the params)
     uint8_t* const ocodes = o ? a.o[1].codes : a.o[0].codes;
     uint8_t* const osf = o ? a.o[1].sf : a.o[0].sf;
@@ -638,11 +617,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const uint64_t ohead = o ? a.o[1].sr_head : a.o[0].sr_head;
     const uint32_t oK = (uint32_t)(o ? a.o[1].K : a.o[0].K);
     const uint32_t okb = (oK + 63) / 64;
-    // the folded signs leave the other rotation's sign on a dual chunk: flip code signs
-    const uint32_t cflip = DUAL ? ((((o ? a.o[0].sign[rt >> 5] : a.o[1].sign[rt >> 5]) >> (rt & 31)) & 1u) ? 0x88888888u : 0u) : 0u;
     unsigned long long* exmax = reinterpret_cast<unsigned long long*>(misc + 16);   // ABSMAX: exact running max
-    int it = 0;
-    uint32_t use0 = 0, use1 = 0;                              // uses of this group's two buffers
+    const int b = slot;                                       // TMEM buffer: Y1 (128 cols) | Y2 (128 cols)
+    uint32_t use = 0;
     const double C64 = TAPE ? __dmul_rn((double)__ldg(a.tape_scale32), a.inv_sqrt) : a.inv_sqrt;
     const float C = (float)C64;
     const float invC = __frcp_ru(C) * 1.0001f;                          // upper bound of 1/C
@@ -650,15 +627,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const double qs = MODE == TC_QUANT ? qscale[o] : 0.0;
     const float isd_lo = qs > 0.0 ? __double2float_rd(__drcp_rd(__dmul_rn(qs, a.s))) : 0.f;
     const float isd_hi = qs > 0.0 ? __double2float_ru(__drcp_ru(__dmul_rn(qs, a.s))) : 0.f;
-    const uint32_t* lane_q = nullptr;
-    (void)lane_q;
-    auto push_deferred = [&](bool want, int t) {
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory"); };
+    auto push_deferred = [&](bool want, int t) {            // warp-collective (h == 0 warps)
       uint32_t need = __ballot_sync(0xFFFFFFFFu, want);
       if (!need) return;
       bool inl = false;
       if (want) {
-        const uint32_t slot = atomicAdd(misc, 1u);
-        if (slot < TC_DEF_CAP) deflist[slot] = ((uint32_t)t << 8) | ((uint32_t)o << 7) | (uint32_t)rt;
+        const uint32_t sl = atomicAdd(misc, 1u);
+        if (sl < TC_DEF_CAP) deflist[sl] = ((uint32_t)t << 8) | ((uint32_t)o << 7) | (uint32_t)rt;
         else inl = true;
       }
       uint32_t todo = __ballot_sync(0xFFFFFFFFu, inl);
@@ -674,267 +650,263 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         ovf |= o2; nanscale |= ns;
       }
     };
+    int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int m = it % TC_META;
-      const bool mine = DUAL || ((it & 1) == wg);
+      const bool mine = DUAL || ((it & 1) == slot);
       mbar_wait_sleep(bar_mfull + 8 * m, (it / TC_META) & 1);
       const uint32_t flags = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES)[0];
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_mempty + 8 * m);
       if (!mine) continue;
-      const bool trc = wg == 0 && rt == 0;
-      if (trc) TC_TR(5);
       const uint32_t tr = a.fc.div((uint32_t)t), tcl = (uint32_t)t - tr * (uint32_t)a.tiles_c;
       const uint32_t r = o == 0 ? tr * 128 + rt : tcl * 128 + rt;        // logical row
       const uint32_t ci = o == 0 ? tcl : tr;                             // chunk along K
       const bool tiny = (flags & 4u) != 0, has_small = (flags & 1u) != 0;
-      const int b0 = DUAL ? wg : 2 * wg, b1 = DUAL ? 2 + wg : 2 * wg + 1;
-      mbar_wait_sleep(bar_tfull + 8 * b0, use0 & 1);
-      mbar_wait_sleep(bar_tfull + 8 * b1, use1 & 1);
-      ++use0;
-      ++use1;
-      if (trc) TC_TR(6);
+      mbar_wait_sleep(bar_tfull + 8 * b, use & 1);
+      ++use;
       tc_fence_after();
-      const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+      const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + 256 * b + 64 * h;   // Y1 of this half; Y2 at +128
       if (a.dbg) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) { mbar_arrive(bar_tempty + 8 * b0); mbar_arrive(bar_tempty + 8 * b1); }
+        if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
         continue;
       }
       // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small),
-      // L1(small) <= ||H.small||_2 (Parseval), plus flush-to-zero slack
+      // L1(small) <= ||H.small||_2 (Parseval; both halves of Y2), plus flush-to-zero slack
       float beta = 0.f;
       if (has_small) {
-        uint64_t s2a = 0, s2b = 0;
+        float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
 #pragma unroll 1
-        for (int pc = 0; pc < 4; ++pc) {
+        for (int pc = 0; pc < 2; ++pc) {
           uint32_t v2[32];
-          const uint32_t a2 = tl + 128 * (pc >> 1 ? b1 : b0) + 64 + 32 * (pc & 1);
-          tmem_ld16(v2, a2);
-          tmem_ld16(v2 + 16, a2 + 16);
+          tmem_ld16(v2, tl + 128 + 32 * pc);
+          tmem_ld16(v2 + 16, tl + 144 + 32 * pc);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const uint64_t y2 = pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]));
-            const uint64_t y3 = pk2(__uint_as_float(v2[i + 2]), __uint_as_float(v2[i + 3]));
-            s2a = ffma2(y2, y2, s2a);
-            s2b = ffma2(y3, y3, s2b);
+            sa = fmaf(__uint_as_float(v2[i]), __uint_as_float(v2[i]), sa);
+            sb = fmaf(__uint_as_float(v2[i + 1]), __uint_as_float(v2[i + 1]), sb);
+            sc = fmaf(__uint_as_float(v2[i + 2]), __uint_as_float(v2[i + 2]), sc);
+            sd = fmaf(__uint_as_float(v2[i + 3]), __uint_as_float(v2[i + 3]), sd);
           }
         }
-        float sa, sb, sc, sd;
-        upk2(s2a, sa, sb);
-        upk2(s2b, sc, sd);
-        const float ss = ((sa + sb) + (sc + sd)) * 1.0001f;
+        xch[h].x = (sa + sb) + (sc + sd);
+        pair_sync();
+        const float ss = (xch[0].x + xch[1].x) * 1.0001f;
         beta = ss > 0.f ? __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f) : 0.f;
       }
       const bool exact_chunk = beta == 0.f && !tiny;          // y64 = fl64(fl64(Y * scale) * c) exactly
       const float betaY = beta * invC;
-      if (trc) TC_TR(7);
       bool defer = tiny;
-      float s4g[8];
-      float numf[8], denf[8];
+      float s4g[4], numf[4], denf[4];
       float ymaxc = 0.f;
       uint32_t pmaxb = 0;
-      uint32_t cw[16];
+      uint32_t cw[8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int b = h ? b1 : b0;
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          const int gi = 4 * h + gg;                          // group 0..7 of the chunk
-          uint32_t v1[16], v2[16];
-          tmem_ld16(v1, tl + 128 * b + 16 * gg);
-          if (has_small) tmem_ld16(v2, tl + 128 * b + 64 + 16 * gg);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (gg == 3) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
-          }
-          float Y[16];
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            if (has_small) {
-              uint64_t s2;
-              asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(pk2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))),
-                  "l"(pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]))));
-              upk2(s2, Y[i], Y[i + 1]);
-            } else {
-              Y[i] = __uint_as_float(v1[i]);
-              Y[i + 1] = __uint_as_float(v1[i + 1]);
-            }
-          }
-          float gm = amax3(Y[0], Y[1], Y[2]), gm2 = amax3(Y[3], Y[4], Y[5]);
-          gm = amax3(gm, Y[6], Y[7]);
-          gm2 = amax3(gm2, Y[8], Y[9]);
-          gm = amax3(gm, Y[10], Y[11]);
-          gm2 = amax3(gm2, Y[12], Y[13]);
-          gm = amax3(gm, Y[14], Y[15]);
-          gm = fmaxf(gm, gm2);
-          numf[gi] = 0.f;
-          denf[gi] = 0.f;
-          s4g[gi] = 0.f;
-          cw[2 * gi] = 0u;
-          cw[2 * gi + 1] = 0u;
-          if (MODE == TC_ABSMAX) { ymaxc = fmaxf(ymaxc, gm); continue; }
-          float mn = amin3(Y[0], Y[1], Y[2]), mn2 = amin3(Y[3], Y[4], Y[5]);
-          mn = amin3(mn, Y[6], Y[7]);
-          mn2 = amin3(mn2, Y[8], Y[9]);
-          mn = amin3(mn, Y[10], Y[11]);
-          mn2 = amin3(mn2, Y[12], Y[13]);
-          mn = amin3(mn, Y[14], Y[15]);
-          mn = fminf(mn, mn2);
-          const float gy = gm * C;                            // ~ gmax
-          const float eg = __fmaf_ru(gy, 0x1p-21f, beta);     // |gy - gmax| bound
-          float d = 0.f, s4 = 0.f;
-          double d64 = 0.0;
-          bool unc = !(gy < 0x1p120f) || (gm == 0.f && beta > 0.f);
-          if (MODE == TC_POSTHOC) {
-            // pseudo = E8M3_RTN(fl64(gmax / s))  (posthoc.py:82-83)
-            const float lo = __fmul_rd(__fsub_rd(gy, eg), is_lo), hi = __fmul_ru(__fadd_ru(gy, eg), is_hi);
-            const uint32_t pl = rne4(fmaxf(lo, 0.f)), ph = rne4(hi);
-            unc |= gm != 0.f && (pl != ph || !(lo >= 0x1p-125f));
-            d = __uint_as_float(pl);
-            s4 = d;
-            d64 = (double)d;
-            pmaxb = max(pmaxb, pl);
-          } else if (qs != 0.0 && gm != 0.f) {
-            // s8 = E4M3_RTN(fl64(gmax / (scale32 * s)))  (quantizers.py:177-178)
-            const float lo = __fmul_rd(__fsub_rd(gy, eg), isd_lo), hi = __fmul_ru(__fadd_ru(gy, eg), isd_hi);
-            uint32_t cl, ch;
-            asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
-                "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
-                : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
-            unc |= cl != ch || !(isd_hi < 0x1p120f);
-            s4 = (float)e4m3_val(cl);
-            d64 = __dmul_rn(e4m3_val(cl), qs);
-            d = (float)d64;                                   // rounded: inside the code margin
-          }
-          s4g[gi] = s4;
-          uint32_t c0 = 0, c1 = 0;
-          if (d > 0.f && !unc) {
-            // codes: q = y / d through cvt (ties-to-even) on the brackets q (1 -+ eps); eps covers
-            // the fp32 roundings (2^-21 |q|) and the small-part bound for |q| >= 1/8; below 1/8
-            // the magnitude code is 0 on both sides and only the sign needs |y| > beta
-            float rd;
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
-            const float invc = C * rd;                          // rcp: <= 1 ulp; inside the 2^-21 budget
-            const float eps = __fmaf_ru(8.02f * beta, rd, 0x1p-21f);
-            unc |= !(mn > betaY);                               // sign of a zero / tiny value: literal path
-            const float il = invc * (1.f - eps), ih = invc * (1.f + eps);
-            const uint64_t il2 = pk2(il, il), ih2 = pk2(ih, ih);
-            uint32_t ca[2], cb[2];
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              float qa[8], qb[8];
-#pragma unroll
-              for (int i = 0; i < 8; i += 2) {
-                const uint64_t y2 = pk2(Y[8 * hf + i], Y[8 * hf + i + 1]);
-                uint64_t ra, rb;
-                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ra) : "l"(y2), "l"(il2));
-                asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rb) : "l"(y2), "l"(ih2));
-                upk2(ra, qa[i], qa[i + 1]);
-                upk2(rb, qb[i], qb[i + 1]);
-              }
-              ca[hf] = e2m1x8(qa);
-              cb[hf] = e2m1x8(qb);
-            }
-            c0 = ca[0];
-            c1 = ca[1];
-            if ((ca[0] ^ cb[0]) | (ca[1] ^ cb[1])) {
-              if (exact_chunk && !unc) {
-                // y64 = fl64(Y * c) (tape: fl64(fl64(Y * scale32) * c)) is the reference's value
-                // (unrolled: Y stays in registers)
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                  const uint32_t sh = 4 * (i & 7);
-                  const uint32_t dm = ((i < 8 ? ca[0] ^ cb[0] : ca[1] ^ cb[1]) >> sh) & 15u;
-                  if (!dm) continue;
-                  const double y64 = TAPE ? __dmul_rn(__dmul_rn((double)Y[i], (double)__ldg(a.tape_scale32)), a.inv_sqrt)
-                                          : __dmul_rn((double)Y[i], C64);
-                  const uint32_t nc = rtn_code_exact(y64, d64);
-                  if (i < 8) c0 = (c0 & ~(15u << sh)) | (nc << sh);
-                  else c1 = (c1 & ~(15u << sh)) | (nc << sh);
-                }
-              } else {
-                unc = true;
-              }
-            }
-            // EDEN partial sums: num += Y^2, den += |Y| |q| (times d per group), 4-long fp32 chains
-            uint64_t na2 = 0, nb2 = 0, qa2 = 0, qb2 = 0;
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-              uint32_t hv[4];
-              e2m1x8_f16s(w ? c1 : c0, hv);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int k = 8 * w + 2 * i;
-                float f0, f1;
-                asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-                    : "=f"(f0), "=f"(f1) : "r"(hv[i]));
-                const uint64_t y2 = pk2(Y[k], Y[k + 1]);        // Y and its code share the sign
-                if (w) { nb2 = ffma2(y2, y2, nb2); qb2 = ffma2(y2, pk2(f0, f1), qb2); }
-                else { na2 = ffma2(y2, y2, na2); qa2 = ffma2(y2, pk2(f0, f1), qa2); }
-              }
-            }
-            uint64_t n2, q2;
-            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(n2) : "l"(na2), "l"(nb2));
-            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(qa2), "l"(qb2));
-            float n0, n1, d0, d1;
-            upk2(n2, n0, n1);
-            upk2(q2, d0, d1);
-            numf[gi] = n0 + n1;
-            denf[gi] = d0 + d1;
-          } else {
-            uint64_t n2a = 0, n2b = 0;
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const uint64_t y2 = pk2(Y[i], Y[i + 1]), y3 = pk2(Y[i + 2], Y[i + 3]);
-              n2a = ffma2(y2, y2, n2a);
-              n2b = ffma2(y3, y3, n2b);
-            }
-            float n0, n1, n2, n3;
-            upk2(n2a, n0, n1);
-            upk2(n2b, n2, n3);
-            numf[gi] = (n0 + n1) + (n2 + n3);
-          }
-          if (unc) defer = true;
-          cw[2 * gi] = c0 ^ (d > 0.f ? cflip : 0u);
-          cw[2 * gi + 1] = c1 ^ (d > 0.f ? cflip : 0u);
+      for (int gg = 0; gg < 4; ++gg) {
+        uint32_t v1[16], v2[16];
+        tmem_ld16(v1, tl + 16 * gg);
+        if (has_small) tmem_ld16(v2, tl + 128 + 16 * gg);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (gg == 3) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
         }
+        float Y[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          if (has_small) {
+            uint64_t s2;
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(pk2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))),
+                "l"(pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]))));
+            upk2(s2, Y[i], Y[i + 1]);
+          } else {
+            Y[i] = __uint_as_float(v1[i]);
+            Y[i + 1] = __uint_as_float(v1[i + 1]);
+          }
+        }
+        float gm = amax3(Y[0], Y[1], Y[2]), gm2 = amax3(Y[3], Y[4], Y[5]);
+        gm = amax3(gm, Y[6], Y[7]);
+        gm2 = amax3(gm2, Y[8], Y[9]);
+        gm = amax3(gm, Y[10], Y[11]);
+        gm2 = amax3(gm2, Y[12], Y[13]);
+        gm = amax3(gm, Y[14], Y[15]);
+        gm = fmaxf(gm, gm2);
+        numf[gg] = 0.f;
+        denf[gg] = 0.f;
+        s4g[gg] = 0.f;
+        cw[2 * gg] = 0u;
+        cw[2 * gg + 1] = 0u;
+        if (MODE == TC_ABSMAX) { ymaxc = fmaxf(ymaxc, gm); continue; }
+        float mn = amin3(Y[0], Y[1], Y[2]), mn2 = amin3(Y[3], Y[4], Y[5]);
+        mn = amin3(mn, Y[6], Y[7]);
+        mn2 = amin3(mn2, Y[8], Y[9]);
+        mn = amin3(mn, Y[10], Y[11]);
+        mn2 = amin3(mn2, Y[12], Y[13]);
+        mn = amin3(mn, Y[14], Y[15]);
+        mn = fminf(mn, mn2);
+        const float gy = gm * C;                            // ~ gmax
+        const float eg = __fmaf_ru(gy, 0x1p-21f, beta);     // |gy - gmax| bound
+        float d = 0.f, s4 = 0.f;
+        double d64 = 0.0;
+        bool unc = !(gy < 0x1p120f) || (gm == 0.f && beta > 0.f);
+        if (MODE == TC_POSTHOC) {
+          // pseudo = E8M3_RTN(fl64(gmax / s))  (posthoc.py:82-83)
+          const float lo = __fmul_rd(__fsub_rd(gy, eg), is_lo), hi = __fmul_ru(__fadd_ru(gy, eg), is_hi);
+          const uint32_t pl = rne4(fmaxf(lo, 0.f)), ph = rne4(hi);
+          unc |= gm != 0.f && (pl != ph || !(lo >= 0x1p-125f));
+          d = __uint_as_float(pl);
+          s4 = d;
+          d64 = (double)d;
+          pmaxb = max(pmaxb, pl);
+        } else if (qs != 0.0 && gm != 0.f) {
+          // s8 = E4M3_RTN(fl64(gmax / (scale32 * s)))  (quantizers.py:177-178)
+          const float lo = __fmul_rd(__fsub_rd(gy, eg), isd_lo), hi = __fmul_ru(__fadd_ru(gy, eg), isd_hi);
+          uint32_t cl, ch;
+          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
+              "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
+              : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
+          unc |= cl != ch || !(isd_hi < 0x1p120f);
+          s4 = (float)e4m3_val(cl);
+          d64 = __dmul_rn(e4m3_val(cl), qs);
+          d = (float)d64;                                   // rounded: inside the code margin
+        }
+        s4g[gg] = s4;
+        uint32_t c0 = 0, c1 = 0;
+        if (d > 0.f && !unc) {
+          // codes: q = y / d through cvt (ties-to-even) on the brackets q (1 -+ eps); eps covers
+          // the fp32 roundings (2^-21 |q|) and the small-part bound for |q| >= 1/8; below 1/8
+          // the magnitude code is 0 on both sides and only the sign needs |y| > beta
+          float rd;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
+          const float invc = C * rd;                          // rcp: <= 1 ulp; inside the 2^-21 budget
+          const float eps = __fmaf_ru(8.02f * beta, rd, 0x1p-21f);
+          unc |= !(mn > betaY);                               // sign of a zero / tiny value: literal path
+          const float il = invc * (1.f - eps), ih = invc * (1.f + eps);
+          const uint64_t il2 = pk2(il, il), ih2 = pk2(ih, ih);
+          uint32_t ca[2], cb[2];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            float qa[8], qb[8];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const uint64_t y2 = pk2(Y[8 * hf + i], Y[8 * hf + i + 1]);
+              uint64_t ra, rb;
+              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ra) : "l"(y2), "l"(il2));
+              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rb) : "l"(y2), "l"(ih2));
+              upk2(ra, qa[i], qa[i + 1]);
+              upk2(rb, qb[i], qb[i + 1]);
+            }
+            ca[hf] = e2m1x8(qa);
+            cb[hf] = e2m1x8(qb);
+          }
+          c0 = ca[0];
+          c1 = ca[1];
+          if ((ca[0] ^ cb[0]) | (ca[1] ^ cb[1])) {
+            if (exact_chunk && !unc) {
+              // y64 = fl64(Y * c) (tape: fl64(fl64(Y * scale32) * c)) is the reference's value
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const uint32_t sh = 4 * (i & 7);
+                const uint32_t dm = ((i < 8 ? ca[0] ^ cb[0] : ca[1] ^ cb[1]) >> sh) & 15u;
+                if (!dm) continue;
+                const double y64 = TAPE ? __dmul_rn(__dmul_rn((double)Y[i], (double)__ldg(a.tape_scale32)), a.inv_sqrt)
+                                        : __dmul_rn((double)Y[i], C64);
+                const uint32_t nc = rtn_code_exact(y64, d64);
+                if (i < 8) c0 = (c0 & ~(15u << sh)) | (nc << sh);
+                else c1 = (c1 & ~(15u << sh)) | (nc << sh);
+              }
+            } else {
+              unc = true;
+            }
+          }
+          // EDEN partial sums: num += Y^2, den += |Y| |q| (times d per group), 4-long fp32 chains
+          uint64_t na2 = 0, nb2 = 0, qa2 = 0, qb2 = 0;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            uint32_t hv[4];
+            e2m1x8_f16s(w ? c1 : c0, hv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int k = 8 * w + 2 * i;
+              float f0, f1;
+              asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+                  : "=f"(f0), "=f"(f1) : "r"(hv[i]));
+              const uint64_t y2 = pk2(Y[k], Y[k + 1]);        // Y and its code share the sign
+              if (w) { nb2 = ffma2(y2, y2, nb2); qb2 = ffma2(y2, pk2(f0, f1), qb2); }
+              else { na2 = ffma2(y2, y2, na2); qa2 = ffma2(y2, pk2(f0, f1), qa2); }
+            }
+          }
+          uint64_t n2, q2;
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(n2) : "l"(na2), "l"(nb2));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(qa2), "l"(qb2));
+          float n0, n1, d0, d1;
+          upk2(n2, n0, n1);
+          upk2(q2, d0, d1);
+          numf[gg] = n0 + n1;
+          denf[gg] = d0 + d1;
+        } else {
+          uint64_t n2a = 0, n2b = 0;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const uint64_t y2 = pk2(Y[i], Y[i + 1]), y3 = pk2(Y[i + 2], Y[i + 3]);
+            n2a = ffma2(y2, y2, n2a);
+            n2b = ffma2(y3, y3, n2b);
+          }
+          float n0, n1, n2, n3;
+          upk2(n2a, n0, n1);
+          upk2(n2b, n2, n3);
+          numf[gg] = (n0 + n1) + (n2 + n3);
+        }
+        if (unc) defer = true;
+        cw[2 * gg] = c0;
+        cw[2 * gg + 1] = c1;
       }
       if (MODE == TC_ABSMAX) {
-        // max |y| of the chunk lies in [yl, yu]; exact for an exact chunk
-        const float yv = ymaxc * C, e = __fmaf_ru(yv, 0x1p-21f, beta);
-        const float yu = __fadd_ru(yv, e), yl = fmaxf(__fsub_rd(yv, e), 0.f);
+        // max |y| of the half-chunk lies in [yl, yu]; exact for an exact chunk
+        const float yv = ymaxc * C, ee = __fmaf_ru(yv, 0x1p-21f, beta);
+        const float yu = __fadd_ru(yv, ee), yl = fmaxf(__fsub_rd(yv, ee), 0.f);
         if (exact_chunk && ymaxc > 0.f) {
           const double ex = TAPE ? __dmul_rn(__dmul_rn((double)ymaxc, (double)__ldg(a.tape_scale32)), a.inv_sqrt)
                                  : __dmul_rn((double)ymaxc, C64);
           atomicMax(exmax + o, (unsigned long long)dbits(ex));
         }
         atomicMax(misc + 4 + o, __float_as_uint(yl));
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");   // the tile's lower bounds are in
+        asm volatile("bar.sync %0, 256;" ::"r"(10 + slot) : "memory");   // the tile's lower bounds are in
         const float Lrun = __uint_as_float(misc[4 + o]);
-        push_deferred(tiny || (!exact_chunk && yu >= Lrun), t);
+        fl2[h] = (tiny || (!exact_chunk && yu >= Lrun)) ? 1u : 0u;
+        pair_sync();
+        const bool want = (fl2[0] | fl2[1]) != 0u;
+        if (h == 0) push_deferred(want, t);
         continue;
       }
-      if (trc) TC_TR(8);
-      // codes of the chunk: 64 bytes
-      if (MODE != TC_ABSMAX) {
-        uint4* cp = reinterpret_cast<uint4*>(ocodes + (size_t)r * (oK / 2) + ci * 64);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cp[i] = make_uint4(cw[4 * i], cw[4 * i + 1], cw[4 * i + 2], cw[4 * i + 3]);
+      // codes of the half-chunk: 32 bytes
+      {
+        uint4* cp = reinterpret_cast<uint4*>(ocodes + (size_t)r * (oK / 2) + ci * 64 + 32 * h);
+        cp[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+        cp[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
       }
-      if (!defer) {
-        // S = num64 / den64 = C * num / den (num = sum Y^2, den = sum d_g sum |Y| |q|).  Relative
-        // bounds: fp32 group sums of positive terms (<= 6 roundings) and the cross-group sums
-        // (<= 7), the rounding of Y (2^-24 |Y|) and the small part (|dY| <= betaY, sum |Y| <=
-        // sqrt(128 num)); then S, v in fp32 (rcp <= 2 ulp, products 1 ulp each)
-        float nf = ((numf[0] + numf[1]) + (numf[2] + numf[3])) + ((numf[4] + numf[5]) + (numf[6] + numf[7]));
-        float df = 0.f;
+      // S = num64 / den64 = C * num / den (num = sum Y^2, den = sum d_g sum |Y| |q|).  Relative
+      // bounds: fp32 group sums of positive terms (<= 6 roundings) and the cross-group sums
+      // (<= 7), the rounding of Y (2^-24 |Y|) and the small part (|dY| <= betaY, sum |Y| <=
+      // sqrt(128 num)); then S, v in fp32 (rcp <= 2 ulp, products 1 ulp each)
+      {
+        const float nh = (numf[0] + numf[1]) + (numf[2] + numf[3]);
+        float dh = 0.f;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) df = fmaf(denf[g], s4g[g] > 0.f ? (MODE == TC_POSTHOC ? s4g[g] : (float)__dmul_rn((double)s4g[g], qs)) : 0.f, df);
+        for (int g = 0; g < 4; ++g)
+          dh = fmaf(denf[g], s4g[g] > 0.f ? (MODE == TC_POSTHOC ? s4g[g] : (float)__dmul_rn((double)s4g[g], qs)) : 0.f, dh);
+        xch[h] = make_float4(xch[h].x, nh, dh, defer ? 1.f : 0.f);
+      }
+      pair_sync();
+      const float4 x0 = xch[0], x1 = xch[1];
+      defer = x0.w != 0.f || x1.w != 0.f;
+      uint32_t srdef = 0u;
+      if (!defer) {
+        const float nf = x0.y + x1.y, df = x0.z + x1.z;
         bool ok = nf > 0x1p-100f && df > 0x1p-100f && nf < 0x1p100f && df < 0x1p100f;
         const bool sure_deg = nf == 0.f && betaY == 0.f;
         float S = 1.f, es = 0.f;
@@ -950,15 +922,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           S = C * nf * rdn;
           es = en + ed + 6.f * 0x1p-24f;
         }
-        if (!ok && !sure_deg) defer = true;
+        if (!ok && !sure_deg) srdef = 1u;
         if (!ok) { S = 1.f; es = 0.f; }
-        if (!defer) {
+        if (!srdef) {
           // SR of v = S * scale value: E4M3-style truncation a, p = (v - a) / ulp and u < p
           // (pack_aword) certified on [v (1 - es), v (1 + es)] against the draw's top 20 bits
-          const uint32_t g0 = r * (oK / GROUP) + ci * 8;
-          uint32_t aws[8];
+          const uint32_t g0 = r * (oK / GROUP) + ci * 8 + 4 * h;
+          uint32_t aws[4];
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
+          for (int g = 0; g < 4; ++g) {
             aws[g] = 0u;
             const float sv = s4g[g];
             if (!(sv > 0.f)) continue;
@@ -967,34 +939,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             const uint64_t u53 = mix64(ohead ^ ((uint64_t)(g0 + g) + GOLDEN)) >> 11;
             const uint32_t u20 = (uint32_t)(u53 >> 33), lo20 = bl & 0xFFFFFu, hi20 = bh & 0xFFFFFu;
             const bool same = (bl >> 20) == (bh >> 20) && lo20 > 0u && bl >= 0x02000000u && bh < 0x7E000000u;
-            if (!same || (u20 >= lo20 && u20 <= hi20)) defer = true;
+            if (!same || (u20 >= lo20 && u20 <= hi20)) srdef = 1u;
             const uint32_t up = u20 < lo20 ? 1u : 0u;
             const int E = (int)(bl >> 23) - 127;
             aws[g] = ((uint32_t)(E + 256) << 7) | (((bl >> 20) & 7u) << 4) | (up << 3);
           }
-          if (!defer) {
+          if (!srdef) {
             if (MODE == TC_POSTHOC) {
-              uint4* ap = reinterpret_cast<uint4*>(oaw + g0);
-              *ap = make_uint4(aws[0] | (aws[1] << 16), aws[2] | (aws[3] << 16), aws[4] | (aws[5] << 16),
-                               aws[6] | (aws[7] << 16));
+              *reinterpret_cast<uint2*>(oaw + g0) = make_uint2(aws[0] | (aws[1] << 16), aws[2] | (aws[3] << 16));
             } else {
-              uint32_t w0 = 0, w1 = 0;
+              uint32_t w0 = 0;
 #pragma unroll
-              for (int g = 0; g < 8; ++g) {
+              for (int g = 0; g < 4; ++g) {
                 bool o2 = false;
-                const uint32_t c = aword_code(aws[g], 0, &o2);
+                w0 |= aword_code(aws[g], 0, &o2) << (8 * g);
                 if (o2) ovf = true;
-                if (g < 4) w0 |= c << (8 * g); else w1 |= c << (8 * (g - 4));
               }
-              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8, okb)) = w0;
-              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8 + 4, okb)) = w1;
+              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8 + 4 * h, okb)) = w0;
             }
           }
         }
       }
+      fl2[h] = srdef;
+      pair_sync();
+      defer = defer || fl2[0] != 0u || fl2[1] != 0u;
       if (MODE == TC_POSTHOC && !defer && pmaxb) atomicMax(misc + 2 + o, pmaxb);
-      push_deferred(defer, t);
-      if (trc) TC_TR(9);
+      if (h == 0) push_deferred(defer, t);
     }
   }
 

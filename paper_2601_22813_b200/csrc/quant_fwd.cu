@@ -419,6 +419,38 @@ __device__ __forceinline__ QuantConst quant_const(float scale32, int ncaps, doub
   return q;
 }
 
+// One group the fast path could not certify: the certified path with exact tie and
+// midpoint resolution, else the literal float64 restatement (kept out of line so the
+// fast path's register budget is not shared with it).
+template <int DT>
+__device__ __noinline__ void quant_resolve(const void* __restrict__ x, uint32_t gid, bool fast_ok, QuantConst qc,
+                                           const float* mids, float scale32, int ncaps, double cap0, double cap1,
+                                           FastDiv fgpr, int64_t gpr, int64_t kpr, uint8_t* __restrict__ codes,
+                                           uint8_t* __restrict__ sf, uint32_t* __restrict__ err) {
+  constexpr int GB = DT == Q2_BF16 ? 32 : 64;
+  uint32_t w[16];
+  const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(x) + (int64_t)gid * GB);
+#pragma unroll
+  for (int q = 0; q < GB / 16; ++q) {
+    const uint4 t = __ldg(src + q);
+    w[4 * q] = t.x; w[4 * q + 1] = t.y; w[4 * q + 2] = t.z; w[4 * q + 3] = t.w;
+  }
+  uint64_t vv[8];
+  const float gmax = unpack_group<DT>(w, vv);
+  auto elem = [&](int k) {
+    return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + (int64_t)gid * GROUP + k))
+                         : __ldg(static_cast<const float*>(x) + (int64_t)gid * GROUP + k);
+  };
+  uint32_t lo = 0, hi = 0, s8 = 0;
+  if (!(fast_ok && gmax > 0.f && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8))) {
+    const uint3 e = quant_group_exact<DT>(x, (int64_t)gid * GROUP, scale32, ncaps, cap0, cap1, err);
+    lo = e.x; hi = e.y; s8 = e.z;
+  }
+  const uint32_t r = fgpr.div(gid), j = gid - r * (uint32_t)gpr;
+  *reinterpret_cast<uint2*>(codes + (int64_t)gid * 8) = make_uint2(lo, hi);
+  sf_store(sf, r, j, kpr, (uint8_t)s8);
+}
+
 // Persistent quantizer: a producer warp streams units of QT contiguous
 // 16-groups into a QNST-deep shared-memory ring with cp.async.bulk (TMA
 // engine); QT consumer threads quantize one group each per unit.  Every
@@ -431,7 +463,7 @@ __device__ __forceinline__ QuantConst quant_const(float scale32, int ncaps, doub
 #ifndef Q2_QMINB
 #define Q2_QMINB 2
 #endif
-constexpr int QT = 256, QNST = 8;
+constexpr int QT = 256, QNST = 4;
 
 template <int DT>
 __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
@@ -456,9 +488,9 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
     if ((threadIdx.x & 31) == 0) {
       int i = 0;
       for (int64_t v = blockIdx.x; v < nunits; v += gridDim.x, ++i) {
-        const int64_t u = nunits - 1 - v;
+        const int64_t u = v;
         const int s = i % QNST;
-        if (i >= QNST) mbar_wait_sleep(empty0 + 8 * s, ((i / QNST) - 1) & 1);
+        if (i >= QNST) mbar_wait(empty0 + 8 * s, ((i / QNST) - 1) & 1);
         const uint32_t bytes = (uint32_t)((total - u * QT < QT ? total - u * QT : QT) * GB);
         mbar_expect_tx(full0 + 8 * s, bytes);
         bulk_load(smem_u32(qsm + s * QT * GB), static_cast<const char*>(x) + u * QT * GB, bytes, full0 + 8 * s);
@@ -474,11 +506,20 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
   float* mids = reinterpret_cast<float*>(qsm + QNST * QT * GB + 128);
   if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
   asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+  // Groups the certified fp32 fast path cannot decide (exact E2M1 ties and E4M3 midpoints,
+  // 2-8% of groups: DESIGN §4) go to a block-local list and are resolved densely -- one
+  // group per consumer thread -- whenever QT of them have accumulated, and at the end.
+  uint32_t* fixcnt = reinterpret_cast<uint32_t*>(qsm + QNST * QT * GB + 128 + 512);
+  uint32_t* fixlist = fixcnt + 4;                             // [2 QT]
+  if (threadIdx.x == 0) *fixcnt = 0;
+  asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+  auto resolve = [&](uint32_t gid) {
+    quant_resolve<DT>(x, gid, fast_ok, qc, mids, scale32, ncaps, cap0, cap1, fgpr, gpr, kpr, codes, sf, err);
+  };
   int i = 0;
-  for (int64_t v = blockIdx.x; v < nunits; v += gridDim.x, ++i) {
-    const int64_t u = nunits - 1 - v;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x, ++i) {
     const int s = i % QNST;
-    mbar_wait_sleep(full0 + 8 * s, (i / QNST) & 1);
+    mbar_wait(full0 + 8 * s, (i / QNST) & 1);
     const int64_t gid = u * QT + threadIdx.x;
     const bool live = gid < total;
     uint32_t w[16];
@@ -492,26 +533,42 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(empty0 + 8 * s);  // slot may be refilled
-    if (!live) continue;
-    uint32_t lo = 0, hi = 0, s8 = 0;
-    uint64_t vv[8];
-    const float gmax = unpack_group<DT>(w, vv);
-    // an all-zero group (or tensor, quantizers.py:219-220): codes 0, scale 0, both errors 0
-    if (amax != 0.f && !(gmax == 0.f && fast_ok)) {
-      auto elem = [&](int k) {            // the (rare) tie test re-reads element k
-        return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + gid * GROUP + k))
-                             : __ldg(static_cast<const float*>(x) + gid * GROUP + k);
-      };
-      const bool ok = fast_ok && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8);
-      if (!ok) {                                              // the literal float64 restatement
-        const uint3 e = quant_group_exact<DT>(x, gid * GROUP, scale32, ncaps, cap0, cap1, err);
-        lo = e.x; hi = e.y; s8 = e.z;
+    bool fix = false;
+    if (live) {
+      uint32_t lo = 0, hi = 0, s8 = 0;
+      uint64_t vv[8];
+      const float gmax = unpack_group<DT>(w, vv);
+      // an all-zero group (or tensor, quantizers.py:219-220): codes 0, scale 0, both errors 0
+      if (amax != 0.f && !(gmax == 0.f && fast_ok)) {
+        auto no_elem = [&](int) { return 0.f; };
+        fix = !(fast_ok && group_certified<false>(vv, gmax, qc, mids, no_elem, lo, hi, s8));
+      }
+      if (!fix) {
+        const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+        *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
+        sf_store(sf, r, j, kpr, (uint8_t)s8);
       }
     }
-    const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
-    *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
-    sf_store(sf, r, j, kpr, (uint8_t)s8);
+    // warp-aggregated append to the block-local list
+    const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fix);
+    if (fm) {
+      uint32_t base = 0;
+      if ((threadIdx.x & 31) == 0) base = atomicAdd(fixcnt, (uint32_t)__popc(fm));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (fix) fixlist[base + __popc(fm & ((1u << (threadIdx.x & 31)) - 1u))] = (uint32_t)gid;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+    const uint32_t n = *fixcnt;
+    if (n >= QT) {                                            // one dense round
+      const uint32_t g = fixlist[n - QT + threadIdx.x];
+      asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+      if (threadIdx.x == 0) *fixcnt = n - QT;
+      resolve(g);
+      asm volatile("bar.sync 1, %0;" ::"n"(QT) : "memory");
+    }
   }
+  const uint32_t n = *fixcnt;
+  if (threadIdx.x < n) resolve(fixlist[threadIdx.x]);
 }
 
 }  // namespace q2
@@ -578,7 +635,7 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, Q2_QMINB * nsm));
   const FastDiv fg((uint32_t)(K / 16));
-  const int smem = QNST * QT * (dtype == Q2_BF16 ? 32 : 64) + 128 + 512;
+  const int smem = QNST * QT * (dtype == Q2_BF16 ? 32 : 64) + 128 + 512 + 16 + 8 * QT;
   static unsigned attr_bf16 = 0, attr_f32 = 0;
   if (!(dtype == Q2_BF16 ? smem_opt_in(quant_fwd_kernel<Q2_BF16>, smem, attr_bf16)
                          : smem_opt_in(quant_fwd_kernel<Q2_F32>, smem, attr_f32)))

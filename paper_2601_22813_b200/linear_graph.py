@@ -254,8 +254,12 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
 
 
 def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_dtype=torch.float32,
-             err=None) -> GradPair:
-    """Backward from the tape and the output gradient (linear_graph.py:277-333)."""
+             err=None, operands: dict | None = None) -> GradPair:
+    """Backward from the tape and the output gradient (linear_graph.py:277-333).
+
+    ``operands``: optional dict that receives the four quantized GEMM operands the call
+    computed ("E", "Wt" for dX; "Et", "Xt" for dW; None where an operand stays dense),
+    for parity checks of the exact tensors the GEMMs consumed."""
     cfg = tape.config
     tokens, in_dim = tape.x_shape
     out_dim = tape.w_shape[0]
@@ -351,6 +355,8 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     else:
         dx = product(qe, qwt, lambda: e2.to(wide), lambda: dense(tape.qW).t(), dx_dtype)
     main.wait_stream(side)
+    if operands is not None:
+        operands.update(E=qe, Wt=qwt, Et=qet, Xt=qxt)
     _keep(main, dw)
     e2.record_stream(side)
     for t in (tape.qX,):
