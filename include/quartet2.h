@@ -167,6 +167,9 @@ int q2_set_msed_engine(int engine);
  * out[0] = 128-chunks quantized, out[1] = chunks whose certification failed and
  * that were recomputed by the literal float64 path.  reset != 0 zeroes them.   */
 int q2_msed_stats(unsigned long long out[2], int reset);
+/* Kernel launches this library issued since load (host counter, incremented per
+ * launch); reset != 0 zeroes it.  Used by bench.py for its gpu_launches figure.  */
+unsigned long long q2_launch_count(int reset);
 
 /* Stochastic-rounding baselines.
  *   q2_quant_sr: quantize_sr (quantizers.py:139-161; ncaps 1, cap0 6) and

@@ -10,12 +10,14 @@ from .quantizers import (GROUP, absmax, GUARDED_SCALE_CAP, FP8_RTN_MARGIN, NVFP4
                          deserialize_nvfp4, quantize_rtn, quantize_rtn_46, serialize_nvfp4, set_error_mode)
 from .ms_eden import (ErNvfp4Tensor, Pass1Reductions, ms_eden_estimate_pair, ms_eden_quantize, msed, msed_dual, msed_dual_posthoc, msed_stats, set_msed_engine,
                       pass1, pass2,
-                      posthoc_quantize, CostReport, KernelCost, cost_model, cost_model_table)
+                      posthoc_quantize)
 from .sr import SquareBlockTensor, quantize_square_block, quantize_sr, quantize_sr_46, rht_sr, sr_operand
 from .linear_graph import (ABLATIONS, GradPair, LayerConfig, LinearTape, PAIR_DW, PAIR_DX, backward, baseline_config,
                            format_config, forward, gemm, gemm_emulated, parse_config)
 from .module import Quartet2Linear, Quartet2LinearFunction, quartet2_linear
 from . import formats  # noqa: F401  (formats.py mirror: encode_fp4_rtn, ..., decode_fp8)
+from . import ops  # noqa: F401  (torch.ops.quartet2.* custom operators)
+from .parallel import ShardedLinearStep, shard_rows, step_seeds
 
 __all__ = [
     "CHUNK", "GROUP", "GUARDED_SCALE_CAP", "FP8_RTN_MARGIN", "SeedPair", "derive_stream", "prng_uniform",
@@ -25,6 +27,5 @@ __all__ = [
     "backward", "gemm", "gemm_emulated", "PAIR_DX", "PAIR_DW", "serialize_nvfp4", "deserialize_nvfp4",
     "quantize_sr", "quantize_sr_46", "absmax", "rht_sr", "sr_operand", "quantize_square_block", "SquareBlockTensor",
     "Quartet2Linear", "Quartet2LinearFunction", "quartet2_linear", "ABLATIONS", "format_config", "parse_config",
-    "prng_signs", "rht_apply", "rht_inverse", "hadamard_128", "CostReport", "KernelCost", "cost_model",
-    "cost_model_table",
+    "prng_signs", "rht_apply", "rht_inverse", "hadamard_128", "ShardedLinearStep", "shard_rows", "step_seeds",
 ]

@@ -25,7 +25,7 @@ EXPORTS = (
     "q2_msed_ws_bytes", "q2_msed_quant", "q2_posthoc_pass1", "q2_posthoc_pass2",
     "q2_msed_dual_posthoc", "q2_msed_dual", "q2_msed_dual_ws_bytes", "q2_msed_stats", "q2_set_msed_engine", "q2_gemm_tn", "q2_dequant", "q2_unpack", "q2_pack",
     "q2_quant_sr_ws_bytes", "q2_quant_sr", "q2_rht_sr_quant", "q2_quant_square_block", "q2_sr_quant_src", "q2_quant_fwd_amax",
-    "q2_rht", "q2_formats", "q2_eden_factors",
+    "q2_rht", "q2_formats", "q2_eden_factors", "q2_launch_count",
 )
 
 
@@ -75,6 +75,7 @@ _SIGS = {
     "q2_rht": (_I, [_P, _I, _I64, _I, _P, _P, _D, _P, _P]),
     "q2_formats": (_I, [_I, _P, _P, _P, _I64, _P, _P, _P, _P]),
     "q2_eden_factors": (_I, [_P, _P, _I64, _P, _P]),
+    "q2_launch_count": (ctypes.c_ulonglong, [_I]),
 }
 
 

@@ -244,6 +244,14 @@ inline bool pdl_enabled() {
   return on != 0;
 }
 
+// Kernel launches issued by this library since load (q2_launch_count): the bench's
+// gpu_launches figure.  One counter per process (inline function, single instance).
+inline unsigned long long& launch_counter() {
+  static unsigned long long n = 0;
+  return n;
+}
+inline void count_launch() { __atomic_fetch_add(&launch_counter(), 1ull, __ATOMIC_RELAXED); }
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -257,6 +265,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

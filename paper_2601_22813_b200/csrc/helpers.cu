@@ -175,6 +175,7 @@ extern "C" int q2_eden_factors(const double* x_rot, const double* x_rtn, int64_t
   if (nchunks < 0) return Q2_EINVAL;
   if (nchunks == 0) return Q2_OK;
   if (!x_rot || !x_rtn || !out) return Q2_EINVAL;
+  count_launch();
   eden_factor_kernel<<<(unsigned)((nchunks + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(x_rot, x_rtn,
                                                                                                       nchunks, out);
   return cudaGetLastError() == cudaSuccess ? Q2_OK : Q2_ECUDA;
@@ -189,6 +190,7 @@ extern "C" int q2_formats(int op, const double* x, const double* u, const uint8_
       (op == FMT_E8M3 && !err))
     return Q2_EINVAL;
   const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  count_launch();
   formats_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(op, x, u, codes_in, n, codes_out, vals_out,
                                                                         err);
   return cudaGetLastError() == cudaSuccess ? Q2_OK : Q2_ECUDA;
@@ -205,6 +207,7 @@ extern "C" int q2_rht(const void* x, int dtype, int64_t n, int chunk, const doub
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto launch = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    count_launch();
     kern<<<blocks, threads, smem, s>>>(x, n, chunk, signs_pre, signs_post, scale, out);
   };
   if (dtype == Q2_BF16) launch(rht_kernel<Q2_BF16>);
@@ -219,6 +222,7 @@ extern "C" int q2_dequant(const q2_nvfp4* t, double* out, void* stream) {
   if (!t || !out || t->K % 16) return Q2_EINVAL;
   int64_t n = t->R * (t->K / 16);
   if (n == 0) return Q2_OK;
+  count_launch();
   dequant_kernel<<<nblocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(t->codes, t->sf, t->scale32, t->R, t->K, out);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
@@ -228,6 +232,7 @@ extern "C" int q2_unpack(const q2_nvfp4* t, uint8_t* fp4, uint8_t* scales8, void
   if (!t || !fp4 || !scales8 || t->K % 16) return Q2_EINVAL;
   int64_t n = t->R * (t->K / 16);
   if (n == 0) return Q2_OK;
+  count_launch();
   unpack_kernel<<<nblocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(t->codes, t->sf, t->R, t->K, fp4, scales8);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
@@ -237,7 +242,15 @@ extern "C" int q2_pack(const uint8_t* fp4, const uint8_t* scales8, const q2_nvfp
   if (!t || !fp4 || !scales8 || t->K % 16) return Q2_EINVAL;
   int64_t n = t->R * (t->K / 16);
   if (n == 0) return Q2_OK;
+  count_launch();
   pack_kernel<<<nblocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(fp4, scales8, t->R, t->K, t->codes, t->sf);
   Q2_CHECK_LAUNCH();
   return Q2_OK;
+}
+
+// Kernel launches issued by the library since load (or since the last reset).
+extern "C" unsigned long long q2_launch_count(int reset) {
+  const unsigned long long n = __atomic_load_n(&q2::launch_counter(), __ATOMIC_RELAXED);
+  if (reset) __atomic_store_n(&q2::launch_counter(), 0ull, __ATOMIC_RELAXED);
+  return n;
 }

@@ -356,6 +356,7 @@ extern "C" int q2_posthoc_pass2(const uint16_t* pseudo_bf16, const double* corr,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t groups = R * (K / 16);
   unsigned blocks = (unsigned)std::max<int64_t>(1, (groups + 255) / 256);
+  count_launch();
   posthoc2_kernel<<<blocks, 256, 0, st>>>(pseudo_bf16, corr, reinterpret_cast<const unsigned long long*>(red),
                                           R, K, prng_head(seed_sr, sr_stream), out->sf, out->scale32, err);
   Q2_CHECK_LAUNCH();

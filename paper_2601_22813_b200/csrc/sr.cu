@@ -219,6 +219,7 @@ extern "C" int q2_quant_sr(const void* x, int dtype, int64_t R, int64_t K, int64
   const int64_t groups = R * (K / 16);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((groups + 255) / 256, 148 * 16));
   const uint64_t h0 = prng_head(seed, stream0), h1 = prng_head(seed, stream1);
+  count_launch();
   if (dtype == Q2_BF16)
     sr_quant_kernel<Q2_BF16><<<blocks, 256, 0, s>>>(x, R, K, ncaps, cap0, cap1, margin, scale_div, amax, h0, h1,
                                                     out->codes, out->sf, out->scale32, err);
@@ -247,6 +248,7 @@ extern "C" int q2_quant_square_block(const void* x, int dtype, int64_t R, int64_
   if (rc) return rc;
   const int64_t tasks = (R / 16) * ((C / 16 + 1) / 2);
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tasks + 7) / 8, 148 * 16));
+  count_launch();
   if (dtype == Q2_BF16)
     sq_quant_kernel<Q2_BF16><<<blocks, 256, 0, s>>>(x, R, C, use46, amax, out->codes, out->sf, out->scale32,
                                                     out_t->codes, out_t->sf, out_t->scale32, scales8);

@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .ms_eden import msed, msed_dual
-from .quantizers import (NVFP4Tensor, _err_word, _finish, as_device_matrix, dequantize, quantize_rtn_46,
+from .quantizers import (NVFP4Tensor, _err_word, _finish, api, as_device_matrix, dequantize, quantize_rtn_46,
                          stream_handle)
 from .rht import CHUNK, SeedPair, derive_stream
 from .sr import SquareBlockTensor, quantize_sr, quantize_sr_46, quantize_square_block, sr_operand
@@ -160,14 +160,20 @@ def gemm(qa: NVFP4Tensor, qb: NVFP4Tensor, out_dtype=torch.float32, out: torch.T
     if qa.K != qb.K:
         raise ValueError(f"inner dimensions disagree: {qa.shape} vs {qb.shape}")
     M, N = qa.R, qb.R
+    if qa.device != qb.device:
+        raise ValueError(f"operands on different devices: {qa.device} vs {qb.device}")
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype, device=qa.device)
+    if out.dtype not in (torch.float32, torch.bfloat16) or out.dim() != 2 or out.stride(-1) != 1:
+        raise ValueError("output must be a 2-D float32/bfloat16 tensor with unit column stride")
+    if tuple(out.shape) != (M, N) or out.device != qa.device or out.stride(0) < N:
+        raise ValueError(f"output must be ({M}, {N}) on {qa.device} with row stride >= {N}, "
+                         f"got {tuple(out.shape)} on {out.device} (stride {out.stride(0)})")
     dt = _lib.Q2_F32 if out.dtype == torch.float32 else _lib.Q2_BF16
-    if out.dtype not in (torch.float32, torch.bfloat16) or out.stride(-1) != 1:
-        raise ValueError("output must be float32/bfloat16 with unit column stride")
     a, b = qa.c(), qb.c()
-    _lib.check(_lib.lib().q2_gemm_tn(ctypes.byref(a), ctypes.byref(b), out.data_ptr(), dt, out.stride(0),
-                                     int(accumulate), stream_handle()), "gemm")
+    with torch.cuda.device(qa.device), torch.cuda.nvtx.range("q2.gemm"):
+        _lib.check(_lib.lib().q2_gemm_tn(ctypes.byref(a), ctypes.byref(b), out.data_ptr(), dt, out.stride(0),
+                                         int(accumulate), stream_handle()), "gemm")
     return out
 
 
@@ -218,6 +224,7 @@ def _check_dims(x_shape, w_shape, cfg: LayerConfig) -> None:
         raise ValueError(f"in dimension {in_dim}: the B200 transposed-tape quantizer needs a multiple of 64")
 
 
+@api
 def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out_dtype=torch.float32,
             err=None):
     """Quantized forward pass; returns (Y, tape) (linear_graph.py:243-256)."""
@@ -253,6 +260,7 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
     return y, LinearTape(qx, qw, xs, ws, cfg)
 
 
+@api
 def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_dtype=torch.float32,
              err=None, operands: dict | None = None) -> GradPair:
     """Backward from the tape and the output gradient (linear_graph.py:277-333).

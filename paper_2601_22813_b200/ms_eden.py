@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .quantizers import (GROUP, NVFP4Tensor, _err_word, _finish, as_device_matrix, stream_handle)
+from .quantizers import (GROUP, NVFP4Tensor, _err_word, _finish, api, as_device_matrix, stream_handle)
 from .rht import CHUNK, INV_SQRT_CHUNK, SeedPair, derive_stream, sign_mask, sr_stream
 
 _MODES = {"exact": _lib.Q2_MSED_EXACT, "pow2": _lib.Q2_MSED_POW2, "posthoc": _lib.Q2_MSED_POSTHOC}
@@ -33,6 +33,7 @@ def _grid_s(s) -> float:
     return s
 
 
+@api
 def msed(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None, mode: str = "exact",
          source: str = "rows", err=None, ws=None) -> NVFP4Tensor:
     """Quantize a logical [R, K] tensor along K with MS-EDEN.
@@ -87,6 +88,7 @@ def msed(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None, mode: 
     return out
 
 
+@api
 def msed_dual(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: int, rot_cols: int, s=6.0,
               mode: str = "exact", err=None):
     """(MS(E), MS(E^T)) from ONE read of a bf16 E [T, N]: the dgrad and wgrad operands
@@ -138,12 +140,14 @@ def msed_stats(reset: bool = False):
     return int(out[0]), int(out[1])
 
 
+@api
 def ms_eden_quantize(x, seeds: SeedPair, s=6.0, tensor_id: int = 0, rotation_id=None,
                      pow2_scale: bool = False) -> NVFP4Tensor:
     """Rotate, RTN with cap 256, EDEN-correct, SR the scales (ms_eden.py:116-153)."""
     return msed(x, seeds, s, tensor_id, rotation_id, "pow2" if pow2_scale else "exact", "rows")
 
 
+@api
 def ms_eden_estimate_pair(a, b, seeds: SeedPair, pair_id: int = 0, s=6.0):
     """Both GEMM operands along their shared inner axis (ms_eden.py:156-180)."""
     if a.shape[-1] != b.shape[-1]:
@@ -184,6 +188,7 @@ class Pass1Reductions:
         return float(self.red[:1].view(torch.float64).item())
 
 
+@api
 def pass1(x, seed_rht: int, s=6.0, tensor_id: int = 0, rotation_id=None):
     """Rotate, quantize against E8M3 pseudo-scales, reduce (posthoc.py:74-95)."""
     s = _grid_s(s)
@@ -208,6 +213,7 @@ def pass1(x, seed_rht: int, s=6.0, tensor_id: int = 0, rotation_id=None):
     return ErNvfp4Tensor(codes, pseudo, shape), Pass1Reductions(red, corr)
 
 
+@api
 def pass2(er: ErNvfp4Tensor, red: Pass1Reductions, seed_sr: int, tensor_id: int = 0) -> NVFP4Tensor:
     """Align pseudo-scales into E4M3: shift, correct, SR (posthoc.py:98-125)."""
     dev = er.codes.device
@@ -221,64 +227,6 @@ def pass2(er: ErNvfp4Tensor, red: Pass1Reductions, seed_sr: int, tensor_id: int 
     _lib.check(rc, "posthoc pass2")
     _finish(err)
     return out
-
-
-@dataclass(frozen=True)
-class KernelCost:
-    """Traffic of one kernel of a re-quantization pipeline (posthoc.py:128-132)."""
-
-    gmem_to_sm_bits_per_elem: float
-    sm_to_gmem_bits_per_elem: float
-    mma_calls_per_group: int
-
-
-@dataclass(frozen=True)
-class CostReport:
-    """Both kernels of a pipeline and their totals (posthoc.py:135-155)."""
-
-    pipeline: str
-    kernel1: KernelCost
-    kernel2: KernelCost
-
-    @property
-    def gmem_to_sm_total(self) -> float:
-        return self.kernel1.gmem_to_sm_bits_per_elem + self.kernel2.gmem_to_sm_bits_per_elem
-
-    @property
-    def sm_to_gmem_total(self) -> float:
-        return self.kernel1.sm_to_gmem_bits_per_elem + self.kernel2.sm_to_gmem_bits_per_elem
-
-    @property
-    def mma_total(self) -> int:
-        return self.kernel1.mma_calls_per_group + self.kernel2.mma_calls_per_group
-
-    @property
-    def total_bits_per_elem(self) -> float:
-        return self.gmem_to_sm_total + self.sm_to_gmem_total
-
-
-def cost_model(pipeline: str, elem_bits: int = 4, scale_bits: int = 8, pseudo_scale_bits: int = 16,
-               group: int = GROUP) -> CostReport:
-    """Bits moved per element by the naive (absmax pass + quantize pass) and the
-    post-hoc (one read writing the extended-range form, then a scales-only pass)
-    re-quantization of an NVFP4 tensor (posthoc.py:158-188).  The B200 post-hoc
-    kernels (``msed64_kernel<…, POSTHOC>`` + ``msed64_pass2_kernel``) follow the
-    post-hoc schedule; their pass 1 also writes one float64 EDEN factor per
-    128-chunk (0.5 bit/elem) that this model, like the reference's, leaves out."""
-    nvfp4 = elem_bits + scale_bits / group
-    er = elem_bits + pseudo_scale_bits / group
-    if pipeline == "naive":
-        return CostReport("naive", KernelCost(nvfp4, 0.0, 1), KernelCost(nvfp4, nvfp4, 1))
-    if pipeline == "posthoc":
-        return CostReport("posthoc", KernelCost(nvfp4, er, 1),
-                          KernelCost(pseudo_scale_bits / group, scale_bits / group, 0))
-    raise ValueError(f"unknown pipeline {pipeline!r}; expected 'naive' or 'posthoc'")
-
-
-def cost_model_table() -> dict:
-    """Both pipelines and the relative bandwidth saving (posthoc.py:191-199)."""
-    naive, post = cost_model("naive"), cost_model("posthoc")
-    return {"naive": naive, "posthoc": post, "saving": 1.0 - post.total_bits_per_elem / naive.total_bits_per_elem}
 
 
 @dataclass

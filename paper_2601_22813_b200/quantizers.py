@@ -10,6 +10,7 @@ exactly representable in float32.
 from __future__ import annotations
 
 import ctypes
+import functools
 import struct
 from dataclasses import dataclass
 
@@ -72,8 +73,39 @@ def check_errors() -> None:
         _raise_bits(bits)
 
 
-def stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _cuda_device_of(args, kw):
+    for a in list(args) + list(kw.values()):
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda:
+                return a.device
+        else:
+            d = getattr(a, "device", None)
+            if isinstance(d, torch.device) and d.type == "cuda":
+                return d
+    return None
+
+
+def api(fn):
+    """Public entry point: an NVTX range named after the reference function, and launches
+    on the device that owns the inputs (torch.cuda.device guard when it is not current)."""
+    name = "q2." + fn.__name__
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        dev = _cuda_device_of(args, kw)
+        with torch.cuda.nvtx.range(name):
+            if dev is None or dev.index is None or dev.index == torch.cuda.current_device():
+                return fn(*args, **kw)
+            with torch.cuda.device(dev):
+                return fn(*args, **kw)
+    return wrapper
+
+
+def stream_handle(device=None) -> int:
+    """The caller's current stream on ``device`` (default: the current device); entry
+    points run under ``torch.cuda.device(tensor.device)`` so launches go to the device
+    that owns the data."""
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 @dataclass
@@ -213,6 +245,7 @@ def _quant_fwd(x, caps, scale_div, err=None, amax=None) -> NVFP4Tensor:
     return out
 
 
+@api
 def absmax(x) -> torch.Tensor:
     """max|x| as a one-element float32 CUDA tensor (the value a fused producer would supply)."""
     x2, _, dt = as_device_matrix(x)
@@ -224,6 +257,7 @@ def absmax(x) -> torch.Tensor:
     return out
 
 
+@api
 def quantize_rtn_46(x, caps=(6.0, 4.0), scale_cap: float = GUARDED_SCALE_CAP, _err=None, amax=None) -> NVFP4Tensor:
     """Forward-pass RTN with per-group Four-over-Six ceiling choice (quantizers.py:206-234).
 
@@ -235,6 +269,7 @@ def quantize_rtn_46(x, caps=(6.0, 4.0), scale_cap: float = GUARDED_SCALE_CAP, _e
     return _quant_fwd(x, caps, caps[0] * scale_cap, _err, amax)
 
 
+@api
 def quantize_rtn(x, s=FP4_ABS_MAX, _err=None) -> NVFP4Tensor:
     """Deterministic NVFP4 quantization with grid ceiling s and cap 256 (quantizers.py:164-181)."""
     s = float(getattr(s, "s", s))
@@ -243,6 +278,7 @@ def quantize_rtn(x, s=FP4_ABS_MAX, _err=None) -> NVFP4Tensor:
     return _quant_fwd(x, (s,), s * 256.0, _err)
 
 
+@api
 def dequantize(t: NVFP4Tensor) -> torch.Tensor:
     """Reconstruct the real-valued tensor, float64 on device (quantizers.py:315-323)."""
     if hasattr(t, "rows") and isinstance(t.rows, NVFP4Tensor):     # SquareBlockTensor: expanded block scales

@@ -115,6 +115,19 @@ def main():
     xq = Q.dequantize(Q.quantize_rtn(xr))
     out.update(eden_xrot=xr, eden_xrtn=xq, eden_S=ME.chunk_correction_factors(xr, xq),
                eden_S1=np.array([ME.correction_factor(xr[0, :128], xq[0, :128])]))
+    # NV4T container bytes (quantizers.py:330-348), dequantize (quantizers.py:315-323) and the
+    # MS-EDEN GEMM-operand pair (ms_eden.py:156-180) on a normal and a wide-range input
+    for tag, fam in (("n", "normal"), ("w", "lognormal_rows")):
+        xs = make(fam, (96, 256), seed=41)
+        t46 = R.quantize_rtn_46(xs)
+        out[f"nv4t_{tag}_x"] = xs
+        out[f"nv4t_{tag}_bytes"] = np.frombuffer(Q.serialize_nvfp4(t46), dtype=np.uint8)
+        out[f"nv4t_{tag}_msed_bytes"] = np.frombuffer(
+            Q.serialize_nvfp4(ME.ms_eden_quantize(xs, seeds, tensor_id=5, rotation_id=6)), dtype=np.uint8)
+        out[f"deq_{tag}"] = Q.dequantize(t46)
+        pa, pb = ME.ms_eden_estimate_pair(xs[:64], xs[32:], seeds, pair_id=RH.derive_stream(1))
+        pack(f"pair_{tag}_a_", pa, out)
+        pack(f"pair_{tag}_b_", pb, out)
     # PRNG known answers
     out["kat_bits"] = np.array([int(RH._bits(0, 0, 0)), int(RH._bits(123, 456, 789))], dtype=np.uint64)
     out["kat_uniform"] = RH.prng_uniform(0, 0, np.arange(4, dtype=np.uint64))

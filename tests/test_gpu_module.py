@@ -70,3 +70,32 @@ def test_trains_a_linear_map(cuda):
         opt.step()
         losses.append(float(loss.detach()))
     assert losses[-1] < 0.1 * losses[0], (losses[0], losses[-1])
+
+
+def test_default_is_reference_quartet2_and_retain_graph(cuda):
+    """The module's default config is baseline_config("quartet2") (exact MS-EDEN), and a
+    second backward through a retained graph gives the same gradients."""
+    q2 = _q2()
+    m = q2.Quartet2Linear(256, 128, device="cuda")
+    assert m.cfg == q2.baseline_config("quartet2")
+    x = torch.randn(128, 256, device="cuda").bfloat16()
+    y = m(x)
+    gy = (1e-2 * torch.randn_like(y.float())).bfloat16()
+    y.backward(gy, retain_graph=True)
+    g1 = m.weight.grad.clone()
+    m.weight.grad = None
+    y.backward(gy)
+    assert torch.equal(m.weight.grad, g1)
+
+
+def test_deferred_errors_no_sync(cuda):
+    """Non-finite input is recorded on the device without raising at the call; the
+    layer's check_errors() raises the reference's ValueError."""
+    q2 = _q2()
+    m = q2.Quartet2Linear(128, 128, device="cuda", check_every=0)
+    x = torch.randn(128, 128, device="cuda").bfloat16()
+    x[3, 5] = float("inf")
+    m(x)                                             # no exception: no host sync in the call
+    with pytest.raises(ValueError, match="finite"):
+        m.check_errors()
+    m.check_errors()                                 # cleared

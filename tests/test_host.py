@@ -103,7 +103,7 @@ def test_module_host_side():
     assert m.weight.shape == (128, 256) and m.weight.dtype == torch.bfloat16 and m.bias.shape == (128,)
     assert m.seeds_for(3) == q2.SeedPair(q2.derive_stream(5, 1, 3), q2.derive_stream(5, 2, 3))
     assert m.seeds_for(0) != q2.Quartet2Linear(256, 128, seed=6).seeds_for(0)
-    assert "posthoc=True" in repr(m)
+    assert "posthoc=False" in repr(m) and m.cfg == q2.baseline_config("quartet2")
 
 
 def test_ablation_config_validation():
@@ -163,27 +163,6 @@ def test_config_text_matches_live_reference(tmp_path):
                 outcomes.append(str(exc))
         assert outcomes[0] == outcomes[1], (text, outcomes)
 
-
-def test_cost_model():
-    """posthoc.py:158-199: naive 4.5 + (4.5 + 4.5) bits/elem, post-hoc (4.5 + 5) + (1 + 0.5)."""
-    import paper_2601_22813_b200 as q2
-    t = q2.cost_model_table()
-    assert t["naive"].total_bits_per_elem == 13.5 and t["naive"].mma_total == 2
-    assert t["posthoc"].total_bits_per_elem == 11.0 and t["posthoc"].mma_total == 1
-    assert abs(t["saving"] - (1 - 11 / 13.5)) < 1e-15
-    with pytest.raises(ValueError, match="expected 'naive' or 'posthoc'"):
-        q2.cost_model("eager")
-    if os.path.isdir("/root/reference/pkg/src"):
-        import sys
-        sys.path.insert(0, "/root/reference/pkg/src")
-        from nvfp4emu import posthoc as PH
-        for args in ((), (4, 8, 16, 32), (2, 8, 8, 16)):
-            for pipe in ("naive", "posthoc"):
-                a, b = q2.cost_model(pipe, *args), PH.cost_model(pipe, *args)
-                assert (a.total_bits_per_elem, a.mma_total, a.gmem_to_sm_total) == \
-                    (b.total_bits_per_elem, b.mma_total, b.gmem_to_sm_total)
-
-
 def test_reports_to_json_stable():
     import json
     import numpy as np
@@ -195,3 +174,23 @@ def test_reports_to_json_stable():
     assert d["mse"][0]["mse_e3"] == 1.5 and d["b"] == [0, 1, 2] and text.endswith("\n")
     with pytest.raises(TypeError, match="not JSON-serializable"):
         H.reports_to_json({"x": object()})
+
+
+def test_custom_ops_fake_shapes():
+    """torch.ops.quartet2.* propagate shapes through FakeTensorMode (no GPU needed):
+    the whole layer written with the custom ops traces to Y [T, out], dX [T, in], dW [out, in]."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    import paper_2601_22813_b200 as q2
+    with FakeTensorMode():
+        x = torch.empty(256, 512, dtype=torch.bfloat16, device="cuda")
+        w = torch.empty(384, 512, dtype=torch.bfloat16, device="cuda")
+        e = torch.empty(256, 384, dtype=torch.bfloat16, device="cuda")
+        codes, sf, scale = torch.ops.quartet2.quantize_rtn_46(x)
+        assert codes.shape == (256, 256) and sf.shape == (q2.ops.sf_bytes(256, 512),) and scale.shape == (1,)
+        y, dx, dw = q2.ops.linear_fwd_bwd(x, w, e, q2.SeedPair(1, 2))
+        assert (y.shape, dx.shape, dw.shape) == ((256, 384), (256, 512), (384, 512))
+        assert y.dtype == torch.bfloat16 and dx.dtype == dw.dtype == torch.float32
+    L = q2._lib.lib()
+    for R, K in ((256, 512), (300, 80), (16384, 11264)):
+        assert q2.ops.sf_bytes(R, K) == L.q2_sf_bytes(R, K)

@@ -1,12 +1,12 @@
-"""Token-sharded data parallelism, host logic on CPU with gloo (world_size 2).
+"""Token-sharded data parallelism, world_size 2 on CPU with gloo.
 
-SURVEY.md §8(e): each rank quantizes and multiplies its token shard locally;
-the only exchange is the fp32 dW all-reduce.  Each shard is an independent
-tensor (own amax / scale32, own seeds), so the reference for the all-reduced
-dW is sum_r backward(forward(X_r, W), E_r, seeds_r).dW computed by the oracle.
-These tests run the oracle per rank (CPU), all-reduce through torch.distributed
-(gloo, 127.0.0.1) and check the exchange reproduces that sum exactly, plus the
-bench's per-rank seed derivation and shard bookkeeping.
+SURVEY.md §8(e): each rank quantizes and multiplies its token shard locally; the
+only exchange is the fp32 dW all-reduce.  These tests run the PRODUCT's step driver
+(paper_2601_22813_b200.parallel.ShardedLinearStep: shard bookkeeping, per-rank
+seeds, async dW all-reduce per projection, wait at the end of the step) under
+gloo on 127.0.0.1, with the CPU oracle injected as the per-shard linear (the
+CUDA kernels need a GPU; their per-shard parity is the -m gpu suite).  The
+all-reduced dW must equal sum_r backward(forward(X_r, W), E_r, seeds_r).dW.
 """
 
 import os
@@ -19,40 +19,51 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SHAPES = ((128, 256), (256, 128))          # (in, out) of two projections
+TOKENS = 256                               # global tokens, split over the ranks
 
 
-def _shard_inputs(rank, tokens=128, din=128, dout=128):
-    rng = np.random.default_rng(1000 + rank)
-    x = rng.standard_normal((tokens, din)).astype(np.float32)
-    e = (1e-2 * rng.standard_normal((tokens, dout))).astype(np.float32)
-    w = (np.random.default_rng(7).standard_normal((dout, din)) / 16).astype(np.float32)   # replicated
-    return x, w, e
+def _global_inputs():
+    rng = np.random.default_rng(1000)
+    data = []
+    for din, dout in SHAPES:
+        x = rng.standard_normal((TOKENS, din)).astype(np.float32)
+        w = (rng.standard_normal((dout, din)) / 16).astype(np.float32)       # replicated
+        e = (1e-2 * rng.standard_normal((TOKENS, dout))).astype(np.float32)
+        data.append((x, w, e))
+    return data
 
 
-def _seeds(rank, step):
+def _oracle_linear(posthoc):
     from oracle import nvfp4_oracle as O
-    return O.SeedPair(O.derive_stream(1, step, rank), O.derive_stream(2, step, rank))
+
+    def fwd(x, w):
+        y, tape = O.forward(x.numpy(), w.numpy())
+        return torch.from_numpy(y), tape
+
+    def bwd(tape, e, seeds):
+        dx, dw = O.backward(tape, e.numpy(), O.SeedPair(seeds.rht, seeds.sr), posthoc=posthoc)
+        return torch.from_numpy(dx), torch.from_numpy(dw.astype(np.float32))
+    return fwd, bwd
 
 
 def _worker(rank, world, port, out_q):
     sys.path.insert(0, ROOT)
-    from oracle import nvfp4_oracle as O
+    from paper_2601_22813_b200.parallel import ShardedLinearStep, shard_rows
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    x, w, e = _shard_inputs(rank)
-    _, tape = O.forward(x, w)
-    dx, dw = O.backward(tape, e, _seeds(rank, 3), posthoc=True)
-    t = torch.from_numpy(dw.astype(np.float32))
-    dist.all_reduce(t)                       # the only collective of the layer
-    g = [torch.zeros(1) for _ in range(world)]
-    dist.all_gather(g, torch.tensor([float(dx.shape[0])]))
+    sl = shard_rows(TOKENS, rank, world)
+    data = [(torch.from_numpy(x[sl]), torch.from_numpy(w), torch.from_numpy(e[sl])) for x, w, e in _global_inputs()]
+    fwd, bwd = _oracle_linear(posthoc=True)
+    runner = ShardedLinearStep(rank=rank, world=world, seed=(1, 2), linear_fwd=fwd, linear_bwd=bwd)
+    out = runner.step(data, 3)
     if rank == 0:
-        out_q.put((t.numpy(), [float(v) for v in g]))
+        out_q.put([dw.numpy() for _, _, dw in out] + [[int(y.shape[0]) for y, _, _ in out]])
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_gloo_token_sharded_wgrad_allreduce():
+def test_gloo_sharded_step_allreduces_wgrad():
     world = 2
     port = 29500 + (os.getpid() % 1000)
     ctx = mp.get_context("spawn")
@@ -60,25 +71,43 @@ def test_gloo_token_sharded_wgrad_allreduce():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    dw, rows = q.get(timeout=300)
+    got = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     sys.path.insert(0, ROOT)
     from oracle import nvfp4_oracle as O
-    ref = np.zeros_like(dw, dtype=np.float64)
-    for r in range(world):
-        x, w, e = _shard_inputs(r)
-        _, tape = O.forward(x, w)
-        ref += O.backward(tape, e, _seeds(r, 3), posthoc=True)[1]
-    np.testing.assert_allclose(dw, ref.astype(np.float32), rtol=1e-6, atol=1e-9)
-    assert rows == [128.0, 128.0]
+    from paper_2601_22813_b200.parallel import shard_rows, step_seeds
+    rows = got.pop()
+    assert rows == [TOKENS // world] * len(SHAPES)
+    for j, (x, w, e) in enumerate(_global_inputs()):
+        ref = np.zeros((w.shape[0], w.shape[1]), np.float64)
+        for r in range(world):
+            sl = shard_rows(TOKENS, r, world)
+            s = step_seeds((1, 2), 3, r)
+            _, tape = O.forward(x[sl], w)
+            ref += O.backward(tape, e[sl], O.SeedPair(s.rht, s.sr), posthoc=True)[1].astype(np.float32)
+        np.testing.assert_allclose(got[j], ref.astype(np.float32), rtol=1e-6, atol=1e-9)
 
 
-def test_rank_seeds_are_distinct_streams():
-    s0, s1 = _seeds(0, 5), _seeds(1, 5)
+def test_step_seeds_distinct_per_rank_and_step():
+    sys.path.insert(0, ROOT)
+    from paper_2601_22813_b200.parallel import step_seeds
+    from paper_2601_22813_b200.rht import derive_stream
+    s0, s1 = step_seeds((1, 2), 5, 0), step_seeds((1, 2), 5, 1)
     assert s0 != s1 and s0.rht != s1.rht and s0.sr != s1.sr
-    assert _seeds(0, 5) == s0                # deterministic per (rank, step)
+    assert step_seeds((1, 2), 5, 0) == s0 != step_seeds((1, 2), 6, 0)
+    assert s0.rht == derive_stream(1, 5, 0) and s0.sr == derive_stream(2, 5, 0)
+
+
+def test_shard_rows():
+    sys.path.insert(0, ROOT)
+    from paper_2601_22813_b200.parallel import shard_rows
+    assert [shard_rows(65536, r, 4) for r in range(4)] == [slice(i * 16384, (i + 1) * 16384) for i in range(4)]
+    with pytest.raises(ValueError):
+        shard_rows(100, 0, 3)
+    with pytest.raises(ValueError):
+        shard_rows(128, 2, 2)
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
