@@ -244,6 +244,19 @@ inline bool pdl_enabled() {
   return on != 0;
 }
 
+// cudaFuncSetAttribute applies to the current device only: opt a kernel into its dynamic
+// shared memory once per device (bit d of done_mask), so a process driving several GPUs
+// launches correctly on each.
+template <class F>
+inline bool smem_opt_in(F* fn, int bytes, unsigned& done_mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return false;
+  if (__atomic_load_n(&done_mask, __ATOMIC_ACQUIRE) & (1u << dev)) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  __atomic_fetch_or(&done_mask, 1u << dev, __ATOMIC_RELEASE);
+  return true;
+}
+
 // Kernel launches issued by this library since load (q2_launch_count): the bench's
 // gpu_launches figure.  One counter per process (inline function, single instance).
 inline unsigned long long& launch_counter() {

@@ -419,13 +419,8 @@ static bool make_sf_map(CUtensorMap* map, const void* sf, int64_t R, int64_t K, 
 
 template <bool F32>
 static int launch_gemm(const CUtensorMap* maps, const GemmArgs& g, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(nvfp4_gemm_kernel<F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM) !=
-        cudaSuccess)
-      return Q2_ECUDA;
-    attr = true;
-  }
+  static unsigned attr = 0;                     // per-device opt-in
+  if (!smem_opt_in(nvfp4_gemm_kernel<F32>, GEMM_SMEM, attr)) return Q2_ECUDA;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -84,12 +84,8 @@ template <int SRC, int DT, int MODE>
 static int launch_m64(const M64Src& s, const M64Args& a, cudaStream_t st) {
   using TL = M64Tile<SRC, DT>;
   auto k = msed64_kernel<SRC, DT, MODE>;
-  static bool attr = false;   // benign race: idempotent
-  if (!attr) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::SMEM) != cudaSuccess)
-      return Q2_ECUDA;
-    attr = true;
-  }
+  static unsigned attr = 0;                     // per-device opt-in
+  if (!smem_opt_in(k, TL::SMEM, attr)) return Q2_ECUDA;
   CUtensorMap tm;
   bool ok;
   if (SRC == Q2_SRC_TAPE_COLS) {
@@ -156,13 +152,8 @@ template <int SRC, int MODE>
 static int launch_tc(const TcArgs& a, int pow2, cudaStream_t st) {
   using LY = TcLayout<SRC == TC_TAPE>;
   auto k = msed_tc_kernel<SRC, MODE>;
-  static int attr_dev = -1;                      // per-device opt-in
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, LY::SMEM) != cudaSuccess) return Q2_ECUDA;
-    attr_dev = dev;
-  }
+  static unsigned attr = 0;                     // per-device opt-in
+  if (!smem_opt_in(k, LY::SMEM, attr)) return Q2_ECUDA;
   CUtensorMap tm;
   bool ok;
   if (SRC == TC_TAPE)

@@ -601,17 +601,6 @@ extern "C" int q2_amax(const void* x, int dtype, int64_t R, int64_t K, int64_t l
 // ws: [0] amax bits (16 bytes; the size formula keeps its old, larger value for ABI stability).
 extern "C" size_t q2_quant_fwd_ws_bytes(int64_t R, int64_t K) { return 16 + 4 * (size_t)R * (size_t)(K / 16); }
 
-// cudaFuncSetAttribute applies to the current device only: opt in once per device.
-template <class F>
-static bool smem_opt_in(F* fn, int bytes, unsigned& done_mask) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32) return false;
-  if (done_mask & (1u << dev)) return true;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
-  done_mask |= 1u << dev;
-  return true;
-}
-
 static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld, int ncaps, double cap0,
                      double cap1, double scale_div, const q2_nvfp4* out, const uint32_t* amax_in, void* ws,
                      uint32_t* err, void* stream) {

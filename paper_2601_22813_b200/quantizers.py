@@ -146,10 +146,13 @@ class NVFP4Tensor:
         R = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
         K = shape[-1]
         nsf = _lib.lib().q2_sf_bytes(R, K)
-        # Scale padding (rows beyond R in the last 256-row block) only feeds GEMM
-        # outputs that are masked, so the buffer needs no zero fill.
+        # Scale padding (rows beyond R in the last 256-row block, K groups beyond K in
+        # the last 64-block) only feeds masked GEMM outputs; it is zeroed anyway so the
+        # buffer's bytes are a function of the input (deterministic serialization,
+        # torch.library.opcheck).  Shapes without padding skip the memset.
+        padded = R % 256 != 0 or K % 64 != 0
         return cls(torch.empty((R, K // 2), dtype=torch.uint8, device=device),
-                   torch.empty(nsf, dtype=torch.uint8, device=device),
+                   (torch.zeros if padded else torch.empty)(nsf, dtype=torch.uint8, device=device),
                    torch.empty(1, dtype=torch.float32, device=device), shape)
 
     # ---- reference-layout views (host numpy) ----
