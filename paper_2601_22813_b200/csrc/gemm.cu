@@ -68,6 +68,7 @@ struct GemmArgs {
   int M, N, K, kb;                                        // kb = ceil(K/64) scale blocks per row block
   int tiles_m, tiles_n, nk;
   int accumulate;
+  int dbg;                                                // timing probes: 1 = scale warps skip their TMEM writes
   unsigned long long* trace;                              // optional timeline probe (pair 0), else nullptr
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -272,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t tsf = tmem + trow + SF_COL + SF_SLOT * s;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
+          if (g.dbg == 1) break;
           const uint4 a4 = *reinterpret_cast<const uint4*>(sfa + 512 * kk + (lane >> 3) * 128 + (lane & 7) * 16);
           const uint4 b0 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + (lane & 7) * 16);
           const uint4 b1 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + 128 + (lane & 7) * 16);
@@ -452,7 +454,8 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
   static unsigned long long* trace = nullptr;
   if (getenv("Q2_GEMM_TRACE") && !trace) cudaMalloc(&trace, 64 * 8 * 8);
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
-             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_TRACE") ? trace : nullptr};
+             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_DBG") ? atoi(getenv("Q2_GEMM_DBG")) : 0,
+             getenv("Q2_GEMM_TRACE") ? trace : nullptr};
   if (g.trace) cudaMemsetAsync(trace, 0, 64 * 8 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int rc = d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);

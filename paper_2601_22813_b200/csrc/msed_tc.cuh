@@ -558,10 +558,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const bool tiny = M != 0u && Ef < 80;                      // tile below 2^-47: literal path for all chunks
       const uint32_t thr = Ef >= 9 ? (uint32_t)(Ef - 8) << 7 : 0u;
       const uint32_t thr2 = thr | (thr << 16);
-      // pass 2: main/small split with the signs folded in
+      // pass 2: main/small split (the absmax pass rotates the raw tile: no split)
       uint32_t anys = 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < (MODE == TC_ABSMAX ? 0 : 16); ++i) {
         const int p = st + 128 * i, sl = p >> 10, row = (p & 1023) >> 3;
         const uint32_t off = sl * 16384 + tc_sw(row, piece);
         const uint4 v = *reinterpret_cast<const uint4*>(mainp + off);
@@ -617,7 +617,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const uint64_t ohead = o ? a.o[1].sr_head : a.o[0].sr_head;
     const uint32_t oK = (uint32_t)(o ? a.o[1].K : a.o[0].K);
     const uint32_t okb = (oK + 63) / 64;
-    unsigned long long* exmax = reinterpret_cast<unsigned long long*>(misc + 16);   // ABSMAX: exact running max
     const int b = slot;                                       // TMEM buffer: Y1 (128 cols) | Y2 (128 cols)
     uint32_t use = 0;
     const double C64 = TAPE ? __dmul_rn((double)__ldg(a.tape_scale32), a.inv_sqrt) : a.inv_sqrt;
@@ -673,6 +672,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
         continue;
       }
+      if (MODE == TC_ABSMAX) {
+        // Absmax pass: the raw tile was rotated in one chain, so |Y^ - Y| <= 32 2^-24 L1(x)
+        // <= 2^-19 ||Y||_2 (Parseval, ||Y||_2 = sqrt(128) ||x||_2 >= L1(x)); a chunk whose upper
+        // bound reaches the CTA's running lower bound of the maximum is recomputed exactly
+        // by the literal warp, so the tensor's exact max |y| is among those (quantizers.py:177).
+        float ym = 0.f, sa = 0.f, sb = 0.f;
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) {
+          uint32_t v1[16];
+          tmem_ld16(v1, tl + 16 * gg);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (gg == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            ym = amax3(ym, __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]));
+            sa = fmaf(__uint_as_float(v1[i]), __uint_as_float(v1[i]), sa);
+            sb = fmaf(__uint_as_float(v1[i + 1]), __uint_as_float(v1[i + 1]), sb);
+          }
+        }
+        xch[h].x = sa + sb;
+        pair_sync();
+        const float ss = (xch[0].x + xch[1].x) * 1.0001f;
+        const float bt = __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.001f), 0x1p-118f), C * 1.0001f);
+        const float yv = ym * C, ee = __fmaf_ru(yv, 0x1p-21f, bt);
+        const float yu = __fadd_ru(yv, ee), yl = fmaxf(__fsub_rd(yv, ee), 0.f);
+        atomicMax(misc + 4 + o, __float_as_uint(yl));
+        asm volatile("bar.sync %0, 256;" ::"r"(10 + slot) : "memory");   // the tile's lower bounds are in
+        const float Lrun = __uint_as_float(misc[4 + o]);
+        fl2[h] = (tiny || yu >= Lrun) ? 1u : 0u;
+        pair_sync();
+        const bool want = (fl2[0] | fl2[1]) != 0u;
+        if (h == 0) push_deferred(want, t);
+        continue;
+      }
       // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small),
       // L1(small) <= ||H.small||_2 (Parseval; both halves of Y2), plus flush-to-zero slack
       float beta = 0.f;
@@ -701,7 +738,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const float betaY = beta * invC;
       bool defer = tiny;
       float s4g[4], numf[4], denf[4];
-      float ymaxc = 0.f;
       uint32_t pmaxb = 0;
       uint32_t cw[8];
 #pragma unroll
@@ -740,7 +776,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         s4g[gg] = 0.f;
         cw[2 * gg] = 0u;
         cw[2 * gg + 1] = 0u;
-        if (MODE == TC_ABSMAX) { ymaxc = fmaxf(ymaxc, gm); continue; }
         float mn = amin3(Y[0], Y[1], Y[2]), mn2 = amin3(Y[3], Y[4], Y[5]);
         mn = amin3(mn, Y[6], Y[7]);
         mn2 = amin3(mn2, Y[8], Y[9]);
@@ -865,24 +900,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         cw[2 * gg] = c0;
         cw[2 * gg + 1] = c1;
       }
-      if (MODE == TC_ABSMAX) {
-        // max |y| of the half-chunk lies in [yl, yu]; exact for an exact chunk
-        const float yv = ymaxc * C, ee = __fmaf_ru(yv, 0x1p-21f, beta);
-        const float yu = __fadd_ru(yv, ee), yl = fmaxf(__fsub_rd(yv, ee), 0.f);
-        if (exact_chunk && ymaxc > 0.f) {
-          const double ex = TAPE ? __dmul_rn(__dmul_rn((double)ymaxc, (double)__ldg(a.tape_scale32)), a.inv_sqrt)
-                                 : __dmul_rn((double)ymaxc, C64);
-          atomicMax(exmax + o, (unsigned long long)dbits(ex));
-        }
-        atomicMax(misc + 4 + o, __float_as_uint(yl));
-        asm volatile("bar.sync %0, 256;" ::"r"(10 + slot) : "memory");   // the tile's lower bounds are in
-        const float Lrun = __uint_as_float(misc[4 + o]);
-        fl2[h] = (tiny || (!exact_chunk && yu >= Lrun)) ? 1u : 0u;
-        pair_sync();
-        const bool want = (fl2[0] | fl2[1]) != 0u;
-        if (h == 0) push_deferred(want, t);
-        continue;
-      }
       // codes of the half-chunk: 32 bytes
       {
         uint4* cp = reinterpret_cast<uint4*>(ocodes + (size_t)r * (oK / 2) + ci * 64 + 32 * h);
@@ -989,10 +1006,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     ovf |= o2; nanscale |= ns;
   }
   __syncthreads();
-  if (threadIdx.x < 2 && MODE == TC_ABSMAX && ((SRC >> threadIdx.x) & 1)) {
-    const unsigned long long ex = reinterpret_cast<unsigned long long*>(misc + 16)[threadIdx.x];
-    if (ex) atomicMax(a.o[threadIdx.x].red, ex);
-  }
   if (threadIdx.x < 2 && MODE == TC_POSTHOC) {
     const uint32_t pb = misc[2 + threadIdx.x];
     if (pb && ((SRC >> threadIdx.x) & 1)) atomicMax(&a.o[threadIdx.x].red[1], (unsigned long long)dbits((double)__uint_as_float(pb)));

@@ -14,7 +14,7 @@ E = torch.randn(T, out, device=dev).mul_(1e-3).to(torch.bfloat16)
 X = torch.randn(T, 2048, device=dev).to(torch.bfloat16)
 qX = q2.quantize_rtn_46(X)
 sp = q2.SeedPair(1, 2)
-q2.set_msed_engine("tc")
+q2.set_msed_engine(os.environ.get("Q2_ENGINE", "tc"))
 
 
 def timeit(fn, iters=10):
