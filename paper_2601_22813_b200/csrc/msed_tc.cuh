@@ -57,7 +57,7 @@ constexpr int TC_TILE = 32768;                   // 128 x 128 bf16
 constexpr int TC_RAW = 10240;                    // tape raw tile: codes 8 KB + scales 2 KB
 constexpr int TC_NRAW = 3;
 constexpr int TC_META = 4;                       // metadata ring (tile flags)
-constexpr int TC_META_BYTES = 16;
+constexpr int TC_META_BYTES = 48;                // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask
 constexpr int TC_DEF_CAP = 256;
 constexpr int TC_PF = 6;                         // tiles prefetched into L2 ahead of the TMA ring
 // Shared memory: B operands diag(s) H per orientation (32 KB each) | NS stages of main + small (64 KB each) | tape raw ring |
@@ -524,6 +524,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           for (int j = 0; j < 4; ++j)
             *reinterpret_cast<uint4*>(mainp + (qd >> 1) * 16384 + tc_sw(kr, 4 * (qd & 1) + j)) =
                 make_uint4(ov[4 * j], ov[4 * j + 1], ov[4 * j + 2], ov[4 * j + 3]);
+          if (kr == 0) {            // z0 of the 32 chunks (tile columns) whose input 0 is in this quarter
+            uint32_t zm = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              zm |= (((ov[i] & 0x7FFFu) == 0u ? 1u : 0u) | ((ov[i] & 0x7FFF0000u) == 0u ? 2u : 0u)) << (2 * i);
+            metau[5 + qd] = (a.o[1].sign[0] & 1u) ? zm : 0u;   // tape zeros are +0: -0 iff s[0] < 0
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_rawe + 8 * rs);
@@ -535,12 +542,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         if (lane == 0) { mbar_arrive(bar_split + 8 * s); mbar_arrive(bar_mfull + 8 * m); }
         continue;
       }
-      // pass 1: tile max of |x| (bf16 bits)
-      uint32_t mx = 0;
+      // pass 1: tile max of |x| (bf16 bits), and the z0 masks: chunk input 0 (rows: column 0,
+      // cols: row 0 of the tile) is -0 after the orientation's sign s[0] (see the epilogue)
+      uint32_t mx = 0, zrow = 0, zcol = 0;
+      // x * s[0] == -0 iff x == (s[0] < 0 ? +0 : -0)
+      const uint32_t sneg0 = (a.o[0].sign[0] & 1u) ? 0u : 0x8000u, sneg1 = (a.o[1].sign[0] & 1u) ? 0u : 0x8000u;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int p = st + 128 * i, sl = p >> 10, row = (p & 1023) >> 3;
         const uint4 v = *reinterpret_cast<const uint4*>(mainp + sl * 16384 + tc_sw(row, piece));
+        if (!TAPE && sl == 0 && piece == 0 && (v.x & 0xFFFFu) == sneg0) zrow |= 1u << (i & 31);
+        if (!TAPE && row == 0) {
+          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (((vv[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) == sneg1) zcol |= 1u << (8 * (i >> 3) + e);
+        }
         uint32_t m2;
         asm("max.u16x2 %0, %1, %2;" : "=r"(m2) : "r"(v.x & 0x7FFF7FFFu), "r"(v.y & 0x7FFF7FFFu));
         asm("max.u16x2 %0, %0, %1;" : "+r"(m2) : "r"(v.z & 0x7FFF7FFFu));
@@ -551,12 +568,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
       if (lane == 0) misc[8 + sw] = mx;
+      if (!TAPE && st < 8) metau[1 + st] = 0u;
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (!TAPE) {
+        // rows: thread st (piece 0) saw rows st/8 + 16 i at bit i; cols: thread st < 8 saw columns
+        // 64 (i/8) + 8 st + e at bit 8 (i/8) + e
+        if (zrow)
+          for (int i = 0; i < 8; ++i)
+            if ((zrow >> i) & 1u) { const int r = st / 8 + 16 * i; atomicOr(&metau[1 + (r >> 5)], 1u << (r & 31)); }
+        if (zcol)
+          for (int b = 0; b < 16; ++b)
+            if ((zcol >> b) & 1u) { const int c = 64 * (b >> 3) + 8 * st + (b & 7); atomicOr(&metau[5 + (c >> 5)], 1u << (c & 31)); }
+      }
       const uint32_t M = max(max(misc[8], misc[9]), max(misc[10], misc[11]));
       const int Ef = (int)(M >> 7);                              // biased binade of the tile max
       const bool nonfin = M >= 0x7F80u;
       const bool tiny = M != 0u && Ef < 80;                      // tile below 2^-47: literal path for all chunks
-      const uint32_t thr = Ef >= 9 ? (uint32_t)(Ef - 8) << 7 : 0u;
+      // main values lie on the 2^(E-15) grid: bf16 (8 significant bits) from 2^(E-8), the decoded
+      // tape (FP4 x E4M3: <= 6 significant bits) from 2^(E-10)
+      constexpr int SPLIT = TAPE ? 10 : 8;
+      const uint32_t thr = Ef >= SPLIT + 1 ? (uint32_t)(Ef - SPLIT) << 7 : 0u;
       const uint32_t thr2 = thr | (thr << 16);
       // pass 2: main/small split (the absmax pass rotates the raw tile: no split)
       uint32_t anys = 0;
@@ -654,7 +685,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const int m = it % TC_META;
       const bool mine = DUAL || ((it & 1) == slot);
       mbar_wait_sleep(bar_mfull + 8 * m, (it / TC_META) & 1);
-      const uint32_t flags = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES)[0];
+      const uint32_t* meta = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES);
+      const uint32_t flags = meta[0];
+      // z0: input 0 of this chunk is -0 after the rotation sign.  Only then can an exactly
+      // zero output of the reference's butterflies be -0 (every output's left operand chain
+      // ends at input 0; a zero from cancellation is +0), i.e. carry code sign 1.
+      const bool z0 = (meta[(o ? 5 : 1) + (rt >> 5)] >> (rt & 31)) & 1u;
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_mempty + 8 * m);
       if (!mine) continue;
@@ -819,7 +855,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
           const float invc = C * rd;                          // rcp: <= 1 ulp; inside the 2^-21 budget
           const float eps = __fmaf_ru(8.02f * beta, rd, 0x1p-21f);
-          unc |= !(mn > betaY);                               // sign of a zero / tiny value: literal path
+          // sign of a zero / tiny value: literal path -- except an exact zero of an exact chunk
+          // without z0, which is +0 in the reference (the fma below makes it +0 here as well)
+          if (!exact_chunk || z0) unc |= !(mn > betaY);
           const float il = invc * (1.f - eps), ih = invc * (1.f + eps);
           const uint64_t il2 = pk2(il, il), ih2 = pk2(ih, ih);
           uint32_t ca[2], cb[2];
@@ -830,8 +868,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             for (int i = 0; i < 8; i += 2) {
               const uint64_t y2 = pk2(Y[8 * hf + i], Y[8 * hf + i + 1]);
               uint64_t ra, rb;
-              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(ra) : "l"(y2), "l"(il2));
-              asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rb) : "l"(y2), "l"(ih2));
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(ra) : "l"(y2), "l"(il2), "l"(0ull));   // -0 -> +0
+              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rb) : "l"(y2), "l"(ih2), "l"(0ull));
               upk2(ra, qa[i], qa[i + 1]);
               upk2(rb, qb[i], qb[i + 1]);
             }

@@ -13,6 +13,7 @@ E = torch.randn(T, out, device=dev).mul_(1e-3).to(torch.bfloat16)
 X = torch.randn(T, inp, device=dev).to(torch.bfloat16)
 qX = q2.quantize_rtn_46(X)
 sp = q2.SeedPair(1, 2)
+q2.set_msed_engine(os.environ.get("PROF_ENGINE", "auto"))
 for _ in range(2):
     q2.msed_dual(E, sp, 1, 2, 3, 4, 6.0, mode)
     q2.msed(qX, sp, 6.0, 5, 6, mode, "tape")

@@ -10,6 +10,7 @@ import paper_2601_22813_b200 as q2
 from tests.families import FAMILIES, make
 
 dev = torch.device("cuda:0")
+q2.set_msed_engine(os.environ.get("Q2_ENGINE", "auto"))
 if "--rates" in sys.argv:
     for fam in FAMILIES:
         e = torch.from_numpy(make(fam, (1024, 1024), seed=3)).to(dev).to(torch.bfloat16)
