@@ -139,8 +139,9 @@ static M64Args base_args(const M64Src& s, int64_t R, int64_t K, const uint32_t s
 
 // ------------------------------------------------ tensor-core MS-EDEN launches
 // Engine of q2_msed_quant for single-operand sources: 0 auto (tensor-core kernel for the
-// dual E source only, where it is fastest today; literal float64 kernels otherwise),
-// 1 tensor-core kernel wherever eligible, 2 literal float64 kernels everywhere.
+// dual E source and the NVFP4 tape, where it is fastest; literal float64 kernels for the
+// single-orientation bf16 sources), 1 tensor-core kernel wherever eligible, 2 literal
+// float64 kernels everywhere.
 static int g_msed_engine = -1;
 static int msed_engine() {
   if (g_msed_engine < 0) g_msed_engine = getenv("Q2_MSED_LITERAL") ? 2 : 0;
@@ -245,7 +246,7 @@ extern "C" int q2_msed_quant(const void* x, int dtype, const q2_nvfp4* tape, int
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(ws);
   // tensor-core path: bf16 or tape sources with 128-multiple dims
-  const bool tc_ok = msed_engine() == 1 && R > 0 && K > 0 && R % 128 == 0 && K % 128 == 0 &&
+  const bool tc_ok = (msed_engine() == 1 || (msed_engine() == 0 && src_kind == Q2_SRC_TAPE_COLS)) && R > 0 && K > 0 && R % 128 == 0 && K % 128 == 0 &&
                      (src_kind == Q2_SRC_TAPE_COLS || dtype == Q2_BF16) && R / 128 < (1 << 16) && K / 128 < (1 << 16);
   if (tc_ok) {
     TcArgs ta{};

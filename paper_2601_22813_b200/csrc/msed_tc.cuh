@@ -40,19 +40,21 @@
 //
 // CTA (one per SM, persistent, 448 threads):
 //   warp 0      TMA producer (bf16 tiles) / bulk loads (tape codes + scales)
-//   warp 1      TMEM owner; lane 0 issues the MMAs (4 jobs per dual tile:
-//               rows/cols x two 64-column halves, each Y1 + Y2 = 128 columns)
-//   warps 2-5   split warps: tile max, main/small split + signs (tape: decode
-//               NVFP4 -> bf16 first)
+//   warp 1      TMEM owner; lane 0 issues the MMAs: per tile and orientation
+//               two jobs (64-output halves), each Y1 + Y2 = 2 x 64 columns in
+//               its own TMEM slot, so the next tile's half-0 MMAs overlap the
+//               epilogue's half 1
+//   warps 2-5   split warps: tile max, main/small split (tape: decode NVFP4
+//               -> bf16 first)
 //   warps 6-9   epilogue group 0, warps 10-13 epilogue group 1: one thread
-//               per chunk (TMEM lane), both 64-output jobs.  Dual: group o =
+//               per chunk (TMEM lane), half 0 then half 1.  Dual: group o =
 //               orientation o.  Single orientation: groups alternate tiles.
 namespace q2 {
 
 enum { TC_ABSMAX = 0, TC_QUANT = 1, TC_POSTHOC = 2 };
 enum { TC_ROWS = 1, TC_COLS = 2, TC_DUAL = 3, TC_TAPE = 6 };   // bit 0 rows, bit 1 cols, bit 2 tape
 
-constexpr int TC_THREADS = 704;                  // 6 + 16 epilogue warps
+constexpr int TC_THREADS = 448;                  // 6 + 8 epilogue warps
 constexpr int TC_TILE = 32768;                   // 128 x 128 bf16
 constexpr int TC_RAW = 10240;                    // tape raw tile: codes 8 KB + scales 2 KB
 constexpr int TC_NRAW = 3;
@@ -72,8 +74,8 @@ struct TcLayout {
   static constexpr int OFF_META = OFF_RAW + (TAPE ? TC_NRAW * TC_RAW : 0);
   static constexpr int OFF_DEF = OFF_META + TC_META * TC_META_BYTES;
   static constexpr int OFF_MISC = OFF_DEF + TC_DEF_CAP * 4;
-  static constexpr int OFF_XCH = OFF_MISC + 256;   // epilogue pair exchange: float4 [2][128][2] | u32 [2][128][2]
-  static constexpr int OFF_BAR = OFF_XCH + 8192 + 2048;
+  static constexpr int OFF_S4 = OFF_MISC + 256;    // epilogue group scales: float2 [4][256 threads]
+  static constexpr int OFF_BAR = OFF_S4 + 8192;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 static_assert(TcLayout<false>::SMEM <= 232448 && TcLayout<true>::SMEM <= 232448, "shared memory budget");
@@ -323,10 +325,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
   const uint32_t bar_rawe = smem_u32(bars + 3);               // [3] tape raw slot decoded (4 warps)
   const uint32_t bar_split = smem_u32(bars + 6);              // [NS] split done (4 warps)
   const uint32_t bar_sempty = smem_u32(bars + 9);             // [NS] stage free (MMA commit)
-  const uint32_t bar_tfull = smem_u32(bars + 12);             // [4] accumulator ready
-  const uint32_t bar_tempty = smem_u32(bars + 16);            // [4] accumulator drained (8 warps)
+  const uint32_t bar_tfull = smem_u32(bars + 12);             // [4] TMEM slot (buffer b, half h) = 2b + h ready
+  const uint32_t bar_tempty = smem_u32(bars + 16);            // [4] TMEM slot drained (4 warps)
   const uint32_t bar_mfull = smem_u32(bars + 20);             // [4] tile metadata written (4 warps)
-  const uint32_t bar_mempty = smem_u32(bars + 24);            // [4] tile metadata read (16 warps)
+  const uint32_t bar_mempty = smem_u32(bars + 24);            // [4] tile metadata read (8 warps)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + LY::OFF_MISC);
   // misc: [0] deferred count, [1] tmem base, [2..3] pmax (f32 bits, per orientation), [4..5] running L,
   //       [8..11] split-warp maxima, [12] flags (bit0 nonfinite, bit1 ovf, bit2 nanscale)
@@ -343,9 +345,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(bar_tfull + 8 * b, 1);
-      mbar_init(bar_tempty + 8 * b, 8);
+      mbar_init(bar_tempty + 8 * b, 4);
       mbar_init(bar_mfull + 8 * b, 4);
-      mbar_init(bar_mempty + 8 * b, 16);
+      mbar_init(bar_mempty + 8 * b, 8);
     }
     for (int i = 0; i < 24; ++i) misc[i] = 0;
     mbar_fence_init();
@@ -434,7 +436,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
   } else if (warp == 1) {
     // ----------------------------------------------------------------- MMA
     if (lane == 0) {
-      const uint32_t idk = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      // M = 128 (chunks), N = 64 (one output half), bf16 x bf16 -> f32
+      const uint32_t idk = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
       int it = 0;
       uint32_t ubuf0 = 0, ubuf1 = 0;                         // uses of the two accumulator buffers
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -444,31 +447,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         const uint32_t flags = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + (it % TC_META) * TC_META_BYTES)[0];
         const bool has_small = flags & 1u;
         const uint32_t mainb = smem_u32(smem + LY::OFF_ST + s * 2 * TC_TILE), smallb = mainb + TC_TILE;
+        // buffer b (dual: orientation; single orientation: tile parity) = 256 TMEM columns, two
+        // slots 2b + h of 128 columns: Y1 = H.main (64) | Y2 = H.small (64) of output half h
 #pragma unroll 1
-        for (int jj = 0; jj < NB; ++jj) {
-          // accumulator buffer (256 columns: Y1 = H.main | Y2 = H.small, N = 128 each):
-          // dual: one per orientation; single orientation: alternating tiles
-          const int o = DUAL ? jj : ONLY, buf = DUAL ? jj : (it & 1);
-          const uint32_t ub = buf ? ubuf1 : ubuf0;
-          if (ub > 0) mbar_wait_sleep(bar_tempty + 8 * buf, (ub - 1) & 1);
-          if (buf) ++ubuf1; else ++ubuf0;
-          tc_fence_after();
-          const uint32_t id = idk | (o ? (1u << 15) : 0u);
-          const uint32_t bb = smem_u32(smem + LY::OFF_B + jj * 32768);
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+          for (int jj = 0; jj < NB; ++jj) {
+            const int o = DUAL ? jj : ONLY, buf = DUAL ? jj : (it & 1);
+            const uint32_t ub = buf ? ubuf1 : ubuf0;
+            if (ub > 0) mbar_wait_sleep(bar_tempty + 8 * (2 * buf + h), (ub - 1) & 1);
+            if (h == 1) { if (buf) ++ubuf1; else ++ubuf0; }
+            tc_fence_after();
+            const uint32_t id = idk | (o ? (1u << 15) : 0u);
+            const uint32_t bb = smem_u32(smem + LY::OFF_B + jj * 32768) + 8192 * h;   // B rows 64h..64h+63
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            if (part == 1 && (!has_small || a.dbg == 3)) break;
-            if (a.dbg == 4) break;
-            const uint32_t ab = part ? smallb : mainb;
+            for (int part = 0; part < 2; ++part) {
+              if (part == 1 && (!has_small || a.dbg == 3)) break;
+              if (a.dbg == 4) break;
+              const uint32_t ab = part ? smallb : mainb;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              const uint64_t ad = o == 0 ? desc_sw128(ab + (kk >> 2) * 16384 + (kk & 3) * 32)
-                                         : desc_mn_sw128(ab + kk * 2048, 16384, 1024);
-              const uint64_t bd = desc_sw128(bb + (kk >> 2) * 16384 + (kk & 3) * 32);
-              tc_mma_f16(tmem + 256 * buf + 128 * part, ad, bd, id, kk > 0);
+              for (int kk = 0; kk < 8; ++kk) {
+                const uint64_t ad = o == 0 ? desc_sw128(ab + (kk >> 2) * 16384 + (kk & 3) * 32)
+                                           : desc_mn_sw128(ab + kk * 2048, 16384, 1024);
+                const uint64_t bd = desc_sw128(bb + (kk >> 2) * 16384 + (kk & 3) * 32);
+                tc_mma_f16(tmem + 256 * buf + 128 * h + 64 * part, ad, bd, id, kk > 0);
+              }
             }
+            tc_commit(bar_tfull + 8 * (2 * buf + h));
           }
-          tc_commit(bar_tfull + 8 * buf);
         }
         tc_commit(bar_sempty + 8 * s);
       }
@@ -630,17 +636,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     }
   } else {
     // ----------------------------------------------------------- epilogue
-    // 16 warps.  Warp e = warp - 6 reads TMEM lanes 32q..32q+31 (q = warp & 3; one lane =
-    // one chunk rt), slot = (e >> 2) & 1, half h = e >> 3.  The two threads (h = 0, 1) of a
-    // chunk take its groups 0-3 / 4-7 (the two 64-output jobs) and exchange the Y2 norm, the
-    // EDEN sums and the deferral flags through shared memory (pair barrier 2 + 4 slot + q).
-    // Dual: slot = orientation.  Single orientation: slot = tile parity.
-    const int e = warp - 6, q = warp & 3, slot = (e >> 2) & 1, h = e >> 3;
+    // 8 warps.  Warp e = warp - 6 reads TMEM lanes 32q..32q+31 (q = warp & 3; one lane = one
+    // chunk rt) of buffer grp = e >> 2: half 0 (groups 0-3) from slot 2 grp, then half 1
+    // (groups 4-7) from slot 2 grp + 1; each slot is released as soon as it is read, so the
+    // MMAs of the next tile overlap the rest of this one.  Dual: grp = orientation.  Single
+    // orientation: grp = tile parity.
+    const int e = warp - 6, q = warp & 3, grp = e >> 2;
     const int rt = 32 * q + lane;
-    const int o = DUAL ? slot : ONLY;
-    const uint32_t pbar = 2 + 4 * slot + q;
-    float4* const xch = reinterpret_cast<float4*>(smem + LY::OFF_XCH) + (slot * 128 + rt) * 2;      // [2]
-    uint32_t* const fl2 = reinterpret_cast<uint32_t*>(smem + LY::OFF_XCH + 8192) + (slot * 128 + rt) * 2;
+    const int o = DUAL ? grp : ONLY;
     // per-thread constants of this thread's orientation (no dynamic indexing of the params)
     uint8_t* const ocodes = o ? a.o[1].codes : a.o[0].codes;
     uint8_t* const osf = o ? a.o[1].sf : a.o[0].sf;
@@ -648,7 +651,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const uint64_t ohead = o ? a.o[1].sr_head : a.o[0].sr_head;
     const uint32_t oK = (uint32_t)(o ? a.o[1].K : a.o[0].K);
     const uint32_t okb = (oK + 63) / 64;
-    const int b = slot;                                       // TMEM buffer: Y1 (128 cols) | Y2 (128 cols)
+    const int b = grp;                                        // TMEM buffer: slots 2b (half 0), 2b + 1 (half 1)
+    float2* const s4s = reinterpret_cast<float2*>(smem + LY::OFF_S4) + (threadIdx.x - 192) * 4;   // [4] this thread
     uint32_t use = 0;
     const double C64 = TAPE ? __dmul_rn((double)__ldg(a.tape_scale32), a.inv_sqrt) : a.inv_sqrt;
     const float C = (float)C64;
@@ -657,8 +661,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const double qs = MODE == TC_QUANT ? qscale[o] : 0.0;
     const float isd_lo = qs > 0.0 ? __double2float_rd(__drcp_rd(__dmul_rn(qs, a.s))) : 0.f;
     const float isd_hi = qs > 0.0 ? __double2float_ru(__drcp_ru(__dmul_rn(qs, a.s))) : 0.f;
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory"); };
-    auto push_deferred = [&](bool want, int t) {            // warp-collective (h == 0 warps)
+    auto push_deferred = [&](bool want, int t) {            // warp-collective
       uint32_t need = __ballot_sync(0xFFFFFFFFu, want);
       if (!need) return;
       bool inl = false;
@@ -680,10 +683,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         ovf |= o2; nanscale |= ns;
       }
     };
+    auto release = [&](int h) {                               // slot 2b + h fully read
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_tempty + 8 * (2 * b + h));
+    };
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int m = it % TC_META;
-      const bool mine = DUAL || ((it & 1) == slot);
+      const bool mine = DUAL || ((it & 1) == grp);
       mbar_wait_sleep(bar_mfull + 8 * m, (it / TC_META) & 1);
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES);
       const uint32_t flags = meta[0];
@@ -698,14 +706,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const uint32_t r = o == 0 ? tr * 128 + rt : tcl * 128 + rt;        // logical row
       const uint32_t ci = o == 0 ? tcl : tr;                             // chunk along K
       const bool tiny = (flags & 4u) != 0, has_small = (flags & 1u) != 0;
-      mbar_wait_sleep(bar_tfull + 8 * b, use & 1);
-      ++use;
-      tc_fence_after();
-      const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + 256 * b + 64 * h;   // Y1 of this half; Y2 at +128
+      const uint32_t tb = tmem + ((uint32_t)(32 * q) << 16) + 256 * b;  // slot 2b + h at + 128 h: Y1 | Y2 (+64)
       if (a.dbg) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait_sleep(bar_tfull + 8 * (2 * b + h), use & 1);
+          tc_fence_after();
+          release(h);
+        }
+        ++use;
         continue;
       }
       if (MODE == TC_ABSMAX) {
@@ -715,35 +724,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         // by the literal warp, so the tensor's exact max |y| is among those (quantizers.py:177).
         float ym = 0.f, sa = 0.f, sb = 0.f;
 #pragma unroll
-        for (int gg = 0; gg < 4; ++gg) {
-          uint32_t v1[16];
-          tmem_ld16(v1, tl + 16 * gg);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (gg == 3) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
-          }
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait_sleep(bar_tfull + 8 * (2 * b + h), use & 1);
+          tc_fence_after();
+          uint32_t v1[64];
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) {
+          for (int c = 0; c < 4; ++c) tmem_ld16(v1 + 16 * c, tb + 128 * h + 16 * c);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          release(h);
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
             ym = amax3(ym, __uint_as_float(v1[i]), __uint_as_float(v1[i + 1]));
             sa = fmaf(__uint_as_float(v1[i]), __uint_as_float(v1[i]), sa);
             sb = fmaf(__uint_as_float(v1[i + 1]), __uint_as_float(v1[i + 1]), sb);
           }
         }
-        xch[h].x = sa + sb;
-        pair_sync();
-        const float ss = (xch[0].x + xch[1].x) * 1.0001f;
+        ++use;
+        const float ss = (sa + sb) * 1.0001f;
         const float bt = __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.001f), 0x1p-118f), C * 1.0001f);
         const float yv = ym * C, ee = __fmaf_ru(yv, 0x1p-21f, bt);
         const float yu = __fadd_ru(yv, ee), yl = fmaxf(__fsub_rd(yv, ee), 0.f);
         atomicMax(misc + 4 + o, __float_as_uint(yl));
-        asm volatile("bar.sync %0, 256;" ::"r"(10 + slot) : "memory");   // the tile's lower bounds are in
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");   // the tile's lower bounds are in
         const float Lrun = __uint_as_float(misc[4 + o]);
-        fl2[h] = (tiny || yu >= Lrun) ? 1u : 0u;
-        pair_sync();
-        const bool want = (fl2[0] | fl2[1]) != 0u;
-        if (h == 0) push_deferred(want, t);
+        push_deferred(tiny || yu >= Lrun, t);
         continue;
       }
       // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small),
@@ -752,216 +756,231 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       if (has_small) {
         float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
 #pragma unroll 1
-        for (int pc = 0; pc < 2; ++pc) {
-          uint32_t v2[32];
-          tmem_ld16(v2, tl + 128 + 32 * pc);
-          tmem_ld16(v2 + 16, tl + 144 + 32 * pc);
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait_sleep(bar_tfull + 8 * (2 * b + h), use & 1);
+          tc_fence_after();
+          uint32_t v2[64];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_ld16(v2 + 16 * c, tb + 128 * h + 64 + 16 * c);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
+          for (int i = 0; i < 64; i += 4) {
             sa = fmaf(__uint_as_float(v2[i]), __uint_as_float(v2[i]), sa);
             sb = fmaf(__uint_as_float(v2[i + 1]), __uint_as_float(v2[i + 1]), sb);
             sc = fmaf(__uint_as_float(v2[i + 2]), __uint_as_float(v2[i + 2]), sc);
             sd = fmaf(__uint_as_float(v2[i + 3]), __uint_as_float(v2[i + 3]), sd);
           }
         }
-        xch[h].x = (sa + sb) + (sc + sd);
-        pair_sync();
-        const float ss = (xch[0].x + xch[1].x) * 1.0001f;
+        const float ss = ((sa + sb) + (sc + sd)) * 1.0001f;
         beta = ss > 0.f ? __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f) : 0.f;
       }
       const bool exact_chunk = beta == 0.f && !tiny;          // y64 = fl64(fl64(Y * scale) * c) exactly
+      // the sign of a zero / tiny value needs |Y| > betaY -- except an exact zero of an exact
+      // chunk without z0, which is +0 in the reference (the fma below makes it +0 here as well)
+      const bool sign_chk = !exact_chunk || z0;
       const float betaY = beta * invC;
       bool defer = tiny;
-      float s4g[4], numf[4], denf[4];
+      float nh = 0.f, dh = 0.f;
       uint32_t pmaxb = 0;
-      uint32_t cw[8];
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg) {
-        uint32_t v1[16], v2[16];
-        tmem_ld16(v1, tl + 16 * gg);
-        if (has_small) tmem_ld16(v2, tl + 128 + 16 * gg);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (gg == 3) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_tempty + 8 * b);
+      // group pairs gp = 0..3 (half h = gp / 2); one loop body keeps the kernel's code small
+#pragma unroll 1
+      for (int gp = 0; gp < 4; ++gp) {
+        const int h = gp >> 1;
+        if ((gp & 1) == 0) {
+          mbar_wait_sleep(bar_tfull + 8 * (2 * b + h), use & 1);
+          tc_fence_after();
         }
-        float Y[16];
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          if (has_small) {
-            uint64_t s2;
-            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(pk2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))),
-                "l"(pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]))));
-            upk2(s2, Y[i], Y[i + 1]);
-          } else {
-            Y[i] = __uint_as_float(v1[i]);
-            Y[i + 1] = __uint_as_float(v1[i + 1]);
-          }
-        }
-        float gm = amax3(Y[0], Y[1], Y[2]), gm2 = amax3(Y[3], Y[4], Y[5]);
-        gm = amax3(gm, Y[6], Y[7]);
-        gm2 = amax3(gm2, Y[8], Y[9]);
-        gm = amax3(gm, Y[10], Y[11]);
-        gm2 = amax3(gm2, Y[12], Y[13]);
-        gm = amax3(gm, Y[14], Y[15]);
-        gm = fmaxf(gm, gm2);
-        numf[gg] = 0.f;
-        denf[gg] = 0.f;
-        s4g[gg] = 0.f;
-        cw[2 * gg] = 0u;
-        cw[2 * gg + 1] = 0u;
-        float mn = amin3(Y[0], Y[1], Y[2]), mn2 = amin3(Y[3], Y[4], Y[5]);
-        mn = amin3(mn, Y[6], Y[7]);
-        mn2 = amin3(mn2, Y[8], Y[9]);
-        mn = amin3(mn, Y[10], Y[11]);
-        mn2 = amin3(mn2, Y[12], Y[13]);
-        mn = amin3(mn, Y[14], Y[15]);
-        mn = fminf(mn, mn2);
-        const float gy = gm * C;                            // ~ gmax
-        const float eg = __fmaf_ru(gy, 0x1p-21f, beta);     // |gy - gmax| bound
-        float d = 0.f, s4 = 0.f;
-        double d64 = 0.0;
-        bool unc = !(gy < 0x1p120f) || (gm == 0.f && beta > 0.f);
-        if (MODE == TC_POSTHOC) {
-          // pseudo = E8M3_RTN(fl64(gmax / s))  (posthoc.py:82-83)
-          const float lo = __fmul_rd(__fsub_rd(gy, eg), is_lo), hi = __fmul_ru(__fadd_ru(gy, eg), is_hi);
-          const uint32_t pl = rne4(fmaxf(lo, 0.f)), ph = rne4(hi);
-          unc |= gm != 0.f && (pl != ph || !(lo >= 0x1p-125f));
-          d = __uint_as_float(pl);
-          s4 = d;
-          d64 = (double)d;
-          pmaxb = max(pmaxb, pl);
-        } else if (qs != 0.0 && gm != 0.f) {
-          // s8 = E4M3_RTN(fl64(gmax / (scale32 * s)))  (quantizers.py:177-178)
-          const float lo = __fmul_rd(__fsub_rd(gy, eg), isd_lo), hi = __fmul_ru(__fadd_ru(gy, eg), isd_hi);
-          uint32_t cl, ch;
-          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
-              "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
-              : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
-          unc |= cl != ch || !(isd_hi < 0x1p120f);
-          s4 = (float)e4m3_val(cl);
-          d64 = __dmul_rn(e4m3_val(cl), qs);
-          d = (float)d64;                                   // rounded: inside the code margin
-        }
-        s4g[gg] = s4;
-        uint32_t c0 = 0, c1 = 0;
-        if (d > 0.f && !unc) {
-          // codes: q = y / d through cvt (ties-to-even) on the brackets q (1 -+ eps); eps covers
-          // the fp32 roundings (2^-21 |q|) and the small-part bound for |q| >= 1/8; below 1/8
-          // the magnitude code is 0 on both sides and only the sign needs |y| > beta
-          float rd;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d));
-          const float invc = C * rd;                          // rcp: <= 1 ulp; inside the 2^-21 budget
-          const float eps = __fmaf_ru(8.02f * beta, rd, 0x1p-21f);
-          // sign of a zero / tiny value: literal path -- except an exact zero of an exact chunk
-          // without z0, which is +0 in the reference (the fma below makes it +0 here as well)
-          if (!exact_chunk || z0) unc |= !(mn > betaY);
-          const float il = invc * (1.f - eps), ih = invc * (1.f + eps);
-          const uint64_t il2 = pk2(il, il), ih2 = pk2(ih, ih);
-          uint32_t ca[2], cb[2];
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            float qa[8], qb[8];
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-              const uint64_t y2 = pk2(Y[8 * hf + i], Y[8 * hf + i + 1]);
-              uint64_t ra, rb;
-              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(ra) : "l"(y2), "l"(il2), "l"(0ull));   // -0 -> +0
-              asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rb) : "l"(y2), "l"(ih2), "l"(0ull));
-              upk2(ra, qa[i], qa[i + 1]);
-              upk2(rb, qb[i], qb[i + 1]);
+        {
+          float Yp[32];
+          {
+            uint32_t v1[32], v2[32];
+            const uint32_t ta = tb + 128 * h + 32 * (gp & 1);
+            tmem_ld16(v1, ta);
+            tmem_ld16(v1 + 16, ta + 16);
+            if (has_small) {
+              tmem_ld16(v2, ta + 64);
+              tmem_ld16(v2 + 16, ta + 80);
             }
-            ca[hf] = e2m1x8(qa);
-            cb[hf] = e2m1x8(qb);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (gp & 1) release(h);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              if (has_small) {
+                uint64_t s2;
+                asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(pk2(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))),
+                    "l"(pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]))));
+                upk2(s2, Yp[i], Yp[i + 1]);
+              } else {
+                Yp[i] = __uint_as_float(v1[i]);
+                Yp[i + 1] = __uint_as_float(v1[i + 1]);
+              }
+            }
           }
-          c0 = ca[0];
-          c1 = ca[1];
-          if ((ca[0] ^ cb[0]) | (ca[1] ^ cb[1])) {
-            if (exact_chunk && !unc) {
+          // two groups side by side, branch-free (independent chains the scheduler can
+          // interleave); the rare exact-chunk code fix runs after both
+          float gmv[2], mnv[2], s4v[2], dv[2], numv[2], denv[2];
+          double d64v[2];
+          bool uncv[2], dokv[2];
+          uint32_t c0v[2], c1v[2], mm0[2], mm1[2];
+#pragma unroll
+          for (int gq = 0; gq < 2; ++gq) {
+            const float* Y = Yp + 16 * gq;
+            float gm = amax3(Y[0], Y[1], Y[2]), gm2 = amax3(Y[3], Y[4], Y[5]);
+            float mn = amin3(Y[0], Y[1], Y[2]), mn2 = amin3(Y[3], Y[4], Y[5]);
+            gm = amax3(gm, Y[6], Y[7]);
+            mn = amin3(mn, Y[6], Y[7]);
+            gm2 = amax3(gm2, Y[8], Y[9]);
+            mn2 = amin3(mn2, Y[8], Y[9]);
+            gm = amax3(gm, Y[10], Y[11]);
+            mn = amin3(mn, Y[10], Y[11]);
+            gm2 = amax3(gm2, Y[12], Y[13]);
+            mn2 = amin3(mn2, Y[12], Y[13]);
+            gm = amax3(gm, Y[14], Y[15]);
+            mn = amin3(mn, Y[14], Y[15]);
+            gmv[gq] = fmaxf(gm, gm2);
+            mnv[gq] = fminf(mn, mn2);
+          }
+#pragma unroll
+          for (int gq = 0; gq < 2; ++gq) {
+            const float gm = gmv[gq];
+            const float gy = gm * C;                            // ~ gmax
+            const float eg = __fmaf_ru(gy, 0x1p-21f, beta);     // |gy - gmax| bound
+            float d = 0.f, s4 = 0.f;
+            double d64 = 0.0;
+            bool unc = !(gy < 0x1p120f) || (gm == 0.f && beta > 0.f);
+            if (MODE == TC_POSTHOC) {
+              // pseudo = E8M3_RTN(fl64(gmax / s))  (posthoc.py:82-83)
+              const float lo = __fmul_rd(__fsub_rd(gy, eg), is_lo), hi = __fmul_ru(__fadd_ru(gy, eg), is_hi);
+              const uint32_t pl = rne4(fmaxf(lo, 0.f)), ph = rne4(hi);
+              unc |= gm != 0.f && (pl != ph || !(lo >= 0x1p-125f));
+              d = __uint_as_float(pl);
+              s4 = d;
+              pmaxb = max(pmaxb, pl);
+            } else {
+              // s8 = E4M3_RTN(fl64(gmax / (scale32 * s)))  (quantizers.py:177-178)
+              const float lo = __fmul_rd(__fsub_rd(gy, eg), isd_lo), hi = __fmul_ru(__fadd_ru(gy, eg), isd_hi);
+              uint32_t cl, ch;
+              asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
+                  "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
+                  : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
+              const bool live = qs != 0.0 && gm != 0.f;
+              unc |= live && (cl != ch || !(isd_hi < 0x1p120f));
+              s4 = live ? (float)e4m3_val(cl) : 0.f;
+              d64 = __dmul_rn((double)s4, qs);
+              d = (float)d64;                                   // rounded: inside the code margin
+            }
+            // the sign of a zero / tiny value: |Y| > betaY (see sign_chk)
+            unc |= sign_chk && !(mnv[gq] > betaY);
+            s4v[gq] = s4;
+            dv[gq] = d;
+            d64v[gq] = MODE == TC_POSTHOC ? (double)d : d64;
+            uncv[gq] = unc;
+            dokv[gq] = d > 0.f && !unc;
+          }
+#pragma unroll
+          for (int gq = 0; gq < 2; ++gq) {
+            const float* Y = Yp + 16 * gq;
+            // codes: q = y / d through cvt (ties-to-even) on the brackets q (1 -+ eps); eps covers
+            // the fp32 roundings (2^-21 |q|) and the small-part bound for |q| >= 1/8; below 1/8
+            // the magnitude code is 0 on both sides and only the sign needs |y| > beta.  The
+            // fma with +0 turns an exact -0 into +0.
+            float rd;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(dokv[gq] ? dv[gq] : 1.f));
+            const float invc = C * rd;                          // rcp: <= 1 ulp; inside the 2^-21 budget
+            const float eps = __fmaf_ru(8.02f * beta, rd, 0x1p-21f);
+            const float il = invc * (1.f - eps), ih = invc * (1.f + eps);
+            const uint64_t il2 = pk2(il, il), ih2 = pk2(ih, ih);
+            uint32_t ca[2], cb[2];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              float qa[8], qb[8];
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                const uint64_t y2 = pk2(Y[8 * hf + i], Y[8 * hf + i + 1]);
+                uint64_t ra, rb;
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(ra) : "l"(y2), "l"(il2), "l"(0ull));
+                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rb) : "l"(y2), "l"(ih2), "l"(0ull));
+                upk2(ra, qa[i], qa[i + 1]);
+                upk2(rb, qb[i], qb[i + 1]);
+              }
+              ca[hf] = e2m1x8(qa);
+              cb[hf] = e2m1x8(qb);
+            }
+            const bool ok = dokv[gq];
+            c0v[gq] = ok ? ca[0] : 0u;
+            c1v[gq] = ok ? ca[1] : 0u;
+            mm0[gq] = ok ? ca[0] ^ cb[0] : 0u;
+            mm1[gq] = ok ? ca[1] ^ cb[1] : 0u;
+          }
+          if ((mm0[0] | mm1[0] | mm0[1] | mm1[1]) != 0u) {      // rare: codes on a threshold
+#pragma unroll
+            for (int gq = 0; gq < 2; ++gq) {
+              if (!(mm0[gq] | mm1[gq])) continue;
+              if (!exact_chunk) { uncv[gq] = true; continue; }
               // y64 = fl64(Y * c) (tape: fl64(fl64(Y * scale32) * c)) is the reference's value
+              const float* Y = Yp + 16 * gq;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const uint32_t sh = 4 * (i & 7);
-                const uint32_t dm = ((i < 8 ? ca[0] ^ cb[0] : ca[1] ^ cb[1]) >> sh) & 15u;
-                if (!dm) continue;
+                if (!(((i < 8 ? mm0[gq] : mm1[gq]) >> sh) & 15u)) continue;
                 const double y64 = TAPE ? __dmul_rn(__dmul_rn((double)Y[i], (double)__ldg(a.tape_scale32)), a.inv_sqrt)
                                         : __dmul_rn((double)Y[i], C64);
-                const uint32_t nc = rtn_code_exact(y64, d64);
-                if (i < 8) c0 = (c0 & ~(15u << sh)) | (nc << sh);
-                else c1 = (c1 & ~(15u << sh)) | (nc << sh);
+                const uint32_t nc = rtn_code_exact(y64, d64v[gq]);
+                if (i < 8) c0v[gq] = (c0v[gq] & ~(15u << sh)) | (nc << sh);
+                else c1v[gq] = (c1v[gq] & ~(15u << sh)) | (nc << sh);
               }
-            } else {
-              unc = true;
             }
           }
-          // EDEN partial sums: num += Y^2, den += |Y| |q| (times d per group), 4-long fp32 chains
-          uint64_t na2 = 0, nb2 = 0, qa2 = 0, qb2 = 0;
 #pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            uint32_t hv[4];
-            e2m1x8_f16s(w ? c1 : c0, hv);
+          for (int gq = 0; gq < 2; ++gq) {
+            const float* Y = Yp + 16 * gq;
+            // EDEN partial sums: num += Y^2, den += |Y| |q| (times d per group), 4-long fp32 chains
+            uint64_t na2 = 0, nb2 = 0, qa2 = 0, qb2 = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int k = 8 * w + 2 * i;
-              float f0, f1;
-              asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-                  : "=f"(f0), "=f"(f1) : "r"(hv[i]));
-              const uint64_t y2 = pk2(Y[k], Y[k + 1]);        // Y and its code share the sign
-              if (w) { nb2 = ffma2(y2, y2, nb2); qb2 = ffma2(y2, pk2(f0, f1), qb2); }
-              else { na2 = ffma2(y2, y2, na2); qa2 = ffma2(y2, pk2(f0, f1), qa2); }
+            for (int w = 0; w < 2; ++w) {
+              uint32_t hv[4];
+              e2m1x8_f16s(w ? c1v[gq] : c0v[gq], hv);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int k = 8 * w + 2 * i;
+                float f0, f1;
+                asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+                    : "=f"(f0), "=f"(f1) : "r"(hv[i]));
+                const uint64_t y2 = pk2(Y[k], Y[k + 1]);        // Y and its code share the sign
+                if (w) { nb2 = ffma2(y2, y2, nb2); qb2 = ffma2(y2, pk2(f0, f1), qb2); }
+                else { na2 = ffma2(y2, y2, na2); qa2 = ffma2(y2, pk2(f0, f1), qa2); }
+              }
             }
+            uint64_t n2, q2;
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(n2) : "l"(na2), "l"(nb2));
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(qa2), "l"(qb2));
+            float n0, n1, d0, d1;
+            upk2(n2, n0, n1);
+            upk2(q2, d0, d1);
+            numv[gq] = n0 + n1;
+            denv[gq] = d0 + d1;
           }
-          uint64_t n2, q2;
-          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(n2) : "l"(na2), "l"(nb2));
-          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(q2) : "l"(qa2), "l"(qb2));
-          float n0, n1, d0, d1;
-          upk2(n2, n0, n1);
-          upk2(q2, d0, d1);
-          numf[gg] = n0 + n1;
-          denf[gg] = d0 + d1;
-        } else {
-          uint64_t n2a = 0, n2b = 0;
 #pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            const uint64_t y2 = pk2(Y[i], Y[i + 1]), y3 = pk2(Y[i + 2], Y[i + 3]);
-            n2a = ffma2(y2, y2, n2a);
-            n2b = ffma2(y3, y3, n2b);
+          for (int gq = 0; gq < 2; ++gq) {
+            if (uncv[gq]) defer = true;
+            nh += numv[gq];
+            const float s4 = s4v[gq];
+            dh = fmaf(denv[gq], s4 > 0.f ? (MODE == TC_POSTHOC ? s4 : (float)__dmul_rn((double)s4, qs)) : 0.f, dh);
           }
-          float n0, n1, n2, n3;
-          upk2(n2a, n0, n1);
-          upk2(n2b, n2, n3);
-          numf[gg] = (n0 + n1) + (n2 + n3);
+          s4s[gp] = make_float2(s4v[0], s4v[1]);
+          // codes of the two groups: 16 bytes
+          *reinterpret_cast<uint4*>(ocodes + (size_t)r * (oK / 2) + ci * 64 + 16 * gp) =
+              make_uint4(c0v[0], c1v[0], c0v[1], c1v[1]);
         }
-        if (unc) defer = true;
-        cw[2 * gg] = c0;
-        cw[2 * gg + 1] = c1;
       }
-      // codes of the half-chunk: 32 bytes
-      {
-        uint4* cp = reinterpret_cast<uint4*>(ocodes + (size_t)r * (oK / 2) + ci * 64 + 32 * h);
-        cp[0] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
-        cp[1] = make_uint4(cw[4], cw[5], cw[6], cw[7]);
-      }
+      ++use;
       // S = num64 / den64 = C * num / den (num = sum Y^2, den = sum d_g sum |Y| |q|).  Relative
       // bounds: fp32 group sums of positive terms (<= 6 roundings) and the cross-group sums
       // (<= 7), the rounding of Y (2^-24 |Y|) and the small part (|dY| <= betaY, sum |Y| <=
       // sqrt(128 num)); then S, v in fp32 (rcp <= 2 ulp, products 1 ulp each)
-      {
-        const float nh = (numf[0] + numf[1]) + (numf[2] + numf[3]);
-        float dh = 0.f;
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          dh = fmaf(denf[g], s4g[g] > 0.f ? (MODE == TC_POSTHOC ? s4g[g] : (float)__dmul_rn((double)s4g[g], qs)) : 0.f, dh);
-        xch[h] = make_float4(xch[h].x, nh, dh, defer ? 1.f : 0.f);
-      }
-      pair_sync();
-      const float4 x0 = xch[0], x1 = xch[1];
-      defer = x0.w != 0.f || x1.w != 0.f;
       uint32_t srdef = 0u;
       if (!defer) {
-        const float nf = x0.y + x1.y, df = x0.z + x1.z;
+        const float nf = nh, df = dh;
         bool ok = nf > 0x1p-100f && df > 0x1p-100f && nf < 0x1p100f && df < 0x1p100f;
         const bool sure_deg = nf == 0.f && betaY == 0.f;
         float S = 1.f, es = 0.f;
@@ -982,12 +1001,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         if (!srdef) {
           // SR of v = S * scale value: E4M3-style truncation a, p = (v - a) / ulp and u < p
           // (pack_aword) certified on [v (1 - es), v (1 + es)] against the draw's top 20 bits
-          const uint32_t g0 = r * (oK / GROUP) + ci * 8 + 4 * h;
-          uint32_t aws[4];
+          const uint32_t g0 = r * (oK / GROUP) + ci * 8;
+          uint32_t aws[8];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
+          for (int g = 0; g < 8; ++g) {
             aws[g] = 0u;
-            const float sv = s4g[g];
+            const float sv = g & 1 ? s4s[g >> 1].y : s4s[g >> 1].x;
             if (!(sv > 0.f)) continue;
             const float v = S * sv;
             const uint32_t bl = __float_as_uint(__fmul_rd(v, 1.f - es)), bh = __float_as_uint(__fmul_ru(v, 1.f + es));
@@ -1001,25 +1020,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           }
           if (!srdef) {
             if (MODE == TC_POSTHOC) {
-              *reinterpret_cast<uint2*>(oaw + g0) = make_uint2(aws[0] | (aws[1] << 16), aws[2] | (aws[3] << 16));
+              *reinterpret_cast<uint4*>(oaw + g0) = make_uint4(aws[0] | (aws[1] << 16), aws[2] | (aws[3] << 16),
+                                                               aws[4] | (aws[5] << 16), aws[6] | (aws[7] << 16));
             } else {
-              uint32_t w0 = 0;
+              uint32_t w0 = 0, w1 = 0;
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
-                bool o2 = false;
+                bool o2 = false, o3 = false;
                 w0 |= aword_code(aws[g], 0, &o2) << (8 * g);
-                if (o2) ovf = true;
+                w1 |= aword_code(aws[g + 4], 0, &o3) << (8 * g);
+                if (o2 || o3) ovf = true;
               }
-              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8 + 4 * h, okb)) = w0;
+              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8, okb)) = w0;
+              *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8 + 4, okb)) = w1;
             }
           }
         }
       }
-      fl2[h] = srdef;
-      pair_sync();
-      defer = defer || fl2[0] != 0u || fl2[1] != 0u;
+      defer = defer || srdef != 0u;
       if (MODE == TC_POSTHOC && !defer && pmaxb) atomicMax(misc + 2 + o, pmaxb);
-      if (h == 0) push_deferred(defer, t);
+      push_deferred(defer, t);
     }
   }
 

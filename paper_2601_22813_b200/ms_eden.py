@@ -125,7 +125,7 @@ def msed_dual_posthoc(e, seeds: SeedPair, id_rows: int, rot_rows: int, id_cols: 
 
 
 def set_msed_engine(engine: str) -> None:
-    """``"auto"`` (tensor-core kernel for the dual E source), ``"tc"`` (tensor-core kernel
+    """``"auto"`` (tensor-core kernel for the dual E source and the NVFP4 tape), ``"tc"`` (tensor-core kernel
     wherever eligible) or ``"literal"`` (literal float64 kernels).  Results are identical."""
     code = {"auto": 0, "tc": 1, "literal": 2}[engine]
     _lib.check(_lib.lib().q2_set_msed_engine(code), "q2_set_msed_engine")
