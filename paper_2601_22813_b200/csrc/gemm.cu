@@ -56,6 +56,9 @@ constexpr int SF_COL = 256, SF_SLOT = 48;                 // per stage: 4 x (SFA
 #define Q2_GROUP_M 8
 #endif
 constexpr int GROUP_M = Q2_GROUP_M;
+#ifndef Q2_SF_BATCH
+#define Q2_SF_BATCH 2
+#endif
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;               // shared::cluster address of the leader's copy
 
 // instruction descriptor, kind::mxf4nvf4 (cute InstrDescriptorBlockScaled): a/b E2M1 (=1)
@@ -259,15 +262,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // scale vector; lane L holds rows 32c + L (c = column within a 4-group).
     const int sp = warp - 4;
     const uint32_t trow = (uint32_t)(sp * 32) << 16;
-    int it = 0, tcs = 0;
-    const bool tr = g.trace && pair == 0 && rank == 0 && sp == 0;
-    for (int t = pair; t < ntiles; t += npairs, ++tcs) {
-      unsigned long long wsff = 0, wproc = 0;
-      for (int kt = 0; kt < g.nk; ++kt, ++it) {
-        const int s = it % STAGES;
-        const unsigned long long t0 = tr ? gtime() : 0;
-        mbar_wait_sleep(bar_sff + 8 * s, (it / STAGES) & 1);
-        const unsigned long long t1 = tr ? gtime() : 0;
+    // Stages are written two at a time with one tcgen05.wait::st: the per-stage chain
+    // (LDS -> STTM -> wait -> fence -> remote arrive) is longer than a stage's MMAs, so
+    // one stage per round left the MMA waiting on scales.
+    const int my_tiles = pair < ntiles ? (ntiles - 1 - pair) / npairs + 1 : 0;
+    const int total = my_tiles * g.nk;
+    for (int it = 0; it < total; it += Q2_SF_BATCH) {
+      const int nb = min(Q2_SF_BATCH, total - it);
+#pragma unroll
+      for (int u = 0; u < Q2_SF_BATCH; ++u) {
+        if (u >= nb) break;
+        const int s = (it + u) % STAGES;
+        mbar_wait_sleep(bar_sff + 8 * s, ((it + u) / STAGES) & 1);
         const unsigned char* sfa = smem + s * STAGE + A_ST + B_ST;
         const unsigned char* sfb = sfa + SFA_ST;
         const uint32_t tsf = tmem + trow + SF_COL + SF_SLOT * s;
@@ -283,14 +289,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                        ::"r"(tsf + 12 * kk + 4), "r"(b0.x), "r"(b0.y), "r"(b0.z), "r"(b0.w), "r"(b1.x), "r"(b1.y),
                        "r"(b1.z), "r"(b1.w) : "memory");
         }
-        const unsigned long long t2 = tr ? gtime() : 0;
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_leader(bar_sfr + 8 * s);
-        if (tr) { wsff += t2 - t1; wproc += gtime() - t2; }
       }
-      if (tr && lane == 0 && tcs < 64) { g.trace[384 + 2 * tcs] = wsff; g.trace[385 + 2 * tcs] = wproc; }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        for (int u = 0; u < nb; ++u) mbar_arrive_leader(bar_sfr + 8 * ((it + u) % STAGES));
     }
   } else if (warp >= 8) {
     // ---------------- epilogue ----------------

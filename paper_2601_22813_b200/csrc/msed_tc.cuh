@@ -363,7 +363,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const int k0 = p * 8 + 2 * e, k1 = k0 + 1;
       const uint32_t n0 = (__popc(k0 & j) + (sg[k0 >> 5] >> (k0 & 31))) & 1u;
       const uint32_t n1 = (__popc(k1 & j) + (sg[k1 >> 5] >> (k1 & 31))) & 1u;
-      w[e] = (n0 ? 0xBF80u : 0x3F80u) | ((n1 ? 0xBF80u : 0x3F80u) << 16);
+      const uint32_t one = TAPE ? 0x3C00u : 0x3F80u, mone = TAPE ? 0xBC00u : 0xBF80u;   // +-1 in f16 / bf16
+      w[e] = (n0 ? mone : one) | ((n1 ? mone : one) << 16);
     }
     *reinterpret_cast<uint4*>(smem + LY::OFF_B + bi * 32768 + (p >> 3) * 16384 + tc_sw(j, p & 7)) =
         make_uint4(w[0], w[1], w[2], w[3]);
@@ -437,7 +438,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     // ----------------------------------------------------------------- MMA
     if (lane == 0) {
       // M = 128 (chunks), N = 64 (one output half), bf16 x bf16 -> f32
-      const uint32_t idk = (1u << 4) | (1u << 7) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t ab_fmt = TAPE ? 0u : 1u;                 // f16 (tape) / bf16 operands
+      const uint32_t idk = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
       int it = 0;
       uint32_t ubuf0 = 0, ubuf1 = 0;                         // uses of the two accumulator buffers
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         const unsigned char* raw = smem + LY::OFF_RAW + rs * TC_RAW;
         const int kr = st, L = kr & 31;
 #pragma unroll 1
-        for (int qd = 0; qd < 4; ++qd) {                       // 32 tape columns per quarter
+        for (int qd = 0; qd < (a.dbg == 6 ? 0 : 4); ++qd) {                       // 32 tape columns per quarter
           const uint4 cw = *reinterpret_cast<const uint4*>(raw + kr * 64 + qd * 16);
           const uint32_t sfw = *reinterpret_cast<const uint32_t*>(raw + 8192 + (qd >> 1) * 1024 + ((L >> 3) << 8) +
                                                                   ((tr & 1) << 7) + ((L & 7) << 4) + ((kr >> 5) << 2));
@@ -514,17 +516,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
                 : "h"((unsigned short)(s8 | (s8 << 8))));
           }
           const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
+          // the tape operand is f16: FP4 x E4M3 (2^-10 .. 2688, <= 6 significant bits) is exact
           uint32_t ov[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            uint32_t hv, pv;
+            uint32_t hv;
             asm("{\n\t.reg .b8 t;\n\tcvt.u8.u32 t, %1;\n\tcvt.rn.f16x2.e2m1x2 %0, t;\n\t}" : "=r"(hv) : "r"(ww[i >> 2] >> (8 * (i & 3))));
             // fma with +0 turns the -0 of code 8 into +0 (FP4_VALUES[8] = 0.0)
-            asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(pv) : "r"(hv), "r"(sc[i >> 3]), "r"(0u));
-            float f0, f1;
-            asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-                : "=f"(f0), "=f"(f1) : "r"(pv));
-            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(ov[i]) : "f"(f1), "f"(f0));
+            asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(ov[i]) : "r"(hv), "r"(sc[i >> 3]), "r"(0u));
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -587,13 +586,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             if ((zcol >> b) & 1u) { const int c = 64 * (b >> 3) + 8 * st + (b & 7); atomicOr(&metau[5 + (c >> 5)], 1u << (c & 31)); }
       }
       const uint32_t M = max(max(misc[8], misc[9]), max(misc[10], misc[11]));
-      const int Ef = (int)(M >> 7);                              // biased binade of the tile max
-      const bool nonfin = M >= 0x7F80u;
-      const bool tiny = M != 0u && Ef < 80;                      // tile below 2^-47: literal path for all chunks
+      // biased binade of the tile max (bf16: 8-bit exponent at bit 7; the tape's f16: 5 bits at 10).
+      // Tape values are finite and >= 2^-10 (never tiny).
+      const int Ef = TAPE ? (int)(M >> 10) : (int)(M >> 7);
+      const bool nonfin = !TAPE && M >= 0x7F80u;
+      const bool tiny = !TAPE && M != 0u && Ef < 80;             // tile below 2^-47: literal path for all chunks
       // main values lie on the 2^(E-15) grid: bf16 (8 significant bits) from 2^(E-8), the decoded
       // tape (FP4 x E4M3: <= 6 significant bits) from 2^(E-10)
       constexpr int SPLIT = TAPE ? 10 : 8;
-      const uint32_t thr = Ef >= SPLIT + 1 ? (uint32_t)(Ef - SPLIT) << 7 : 0u;
+      const uint32_t thr = Ef >= SPLIT + 1 ? (uint32_t)(Ef - SPLIT) << (TAPE ? 10 : 7) : 0u;
       const uint32_t thr2 = thr | (thr << 16);
       // pass 2: main/small split (the absmax pass rotates the raw tile: no split)
       uint32_t anys = 0;

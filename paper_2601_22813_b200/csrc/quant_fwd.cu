@@ -571,6 +571,101 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
   if (threadIdx.x < n) resolve(fixlist[threadIdx.x]);
 }
 
+
+// Direct quantizer: every thread streams its 16-groups straight from global memory
+// (32-byte vector loads, the next group's load in flight while the current one is
+// decided), grid-stride in reverse so the tail the amax pass read last is still in
+// L2.  Every decision is settled in the thread: the certified fp32 path with exact
+// E2M1 tie and E4M3 midpoint resolution (run_branch_t<true>: FMA residual against
+// t*E*scale32, Sterbenz-exact difference, even code on a tie), and for the few
+// groups it still cannot certify the literal float64 restatement
+// (quant_group_exact).  No shared-memory ring, no block barriers, no fix-up lists.
+#ifndef Q2_QDMINB
+#define Q2_QDMINB 3
+#endif
+constexpr int QD_THREADS = 256;
+
+template <int DT>
+__device__ __forceinline__ void load_group(const void* x, int64_t gid, bool live, uint32_t (&w)[16]) {
+  if (!live) {
+#pragma unroll
+    for (int i = 0; i < (DT == Q2_BF16 ? 8 : 16); ++i) w[i] = 0u;
+    return;
+  }
+  const char* p = static_cast<const char*>(x) + gid * (DT == Q2_BF16 ? 32 : 64);
+  uint32_t (&a)[8] = *reinterpret_cast<uint32_t(*)[8]>(&w[0]);
+  ld256(p, a);
+  if (DT != Q2_BF16) {
+    uint32_t (&b)[8] = *reinterpret_cast<uint32_t(*)[8]>(&w[8]);
+    ld256(p + 32, b);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel(
+    const void* __restrict__ x, int64_t R, int64_t K, int ncaps, double cap0, double cap1, double scale_div,
+    FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
+    float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
+  __shared__ float mids[128];
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
+  __syncthreads();
+  const float amax = __uint_as_float(*amax_bits);
+  const float scale32 = amax == 0.f ? 0.f : __double2float_rn(__ddiv_rn((double)amax, scale_div));
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scale32_out = scale32;
+  bool fast_ok;
+  const QuantConst qc = quant_const(scale32, ncaps, cap0, cap1, fast_ok);
+  const int64_t gpr = K / GROUP, total = R * gpr, kpr = sf_kblocks(K);
+  const bool quad = (gpr & 3) == 0;                 // 4 consecutive groups share a row: one 32-bit scale store
+  const int64_t nth = (int64_t)gridDim.x * QD_THREADS;
+  const int64_t padded = (total + 31) & ~int64_t(31);
+  const int lane = threadIdx.x & 31;
+  // slot s covers groups [padded - (s + 1) nth, padded - s nth); gid = that base + tid, so
+  // gid = tid (mod 32) and lanes 4m..4m+3 hold four consecutive groups
+  int64_t gid = padded - nth + (int64_t)blockIdx.x * QD_THREADS + threadIdx.x;
+  uint32_t wn[16];
+  load_group<DT>(x, gid, gid >= 0 && gid < total, wn);
+  for (; gid > -nth; gid -= nth) {
+    const bool live = gid >= 0 && gid < total;
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < (DT == Q2_BF16 ? 8 : 16); ++i) w[i] = wn[i];
+    const int64_t nxt = gid - nth;
+    load_group<DT>(x, nxt, nxt >= 0 && nxt < total, wn);
+    uint32_t lo = 0, hi = 0, s8 = 0;
+    if (live && amax != 0.f) {
+      uint64_t vv[8];
+      const float gmax = unpack_group<DT>(w, vv);
+      // an all-zero group (or tensor, quantizers.py:219-220): codes 0, scale 0, both errors 0
+      if (!(gmax == 0.f && fast_ok)) {
+        auto elem = [&](int k) {
+          return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + gid * GROUP + k))
+                               : __ldg(static_cast<const float*>(x) + gid * GROUP + k);
+        };
+        if (!(fast_ok && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8))) {
+          const uint3 e = quant_group_exact<DT>(x, gid * GROUP, scale32, ncaps, cap0, cap1, err);
+          lo = e.x; hi = e.y; s8 = e.z;
+        }
+      }
+    }
+    if (live) *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
+    if (quad) {
+      // lane 4m stores the scales of groups gid .. gid + 3 (same row, j = 0 mod 4)
+      uint32_t wq = s8 << (8 * (lane & 3));
+      wq |= __shfl_xor_sync(0xFFFFFFFFu, wq, 1);
+      wq |= __shfl_xor_sync(0xFFFFFFFFu, wq, 2);
+      if ((lane & 3) == 0 && live) {
+        const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+        *reinterpret_cast<uint32_t*>(sf + sf_offset(r, j, kpr)) = wq;
+      }
+    } else if (live) {
+      const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
+      sf_store(sf, r, j, kpr, (uint8_t)s8);
+    }
+  }
+}
+
 }  // namespace q2
 
 using namespace q2;
@@ -636,7 +731,18 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
   }
   const uint32_t* amax = amax_in ? amax_in : amax_ws;
   cudaError_t e;
-  if (dtype == Q2_BF16)
+  static const int qeng = getenv("Q2_QUANT_DIRECT") ? 1 : 0;   // 1: the direct kernel (A/B timing; slower on small shapes)
+  if (qeng == 1) {
+    const int64_t gthreads = (groups + 31) & ~int64_t(31);
+    const unsigned qblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((gthreads + QD_THREADS - 1) / QD_THREADS,
+                                                                               (int64_t)Q2_QDMINB * nsm));
+    if (dtype == Q2_BF16)
+      e = launch_pdl(quant_fwd_direct_kernel<Q2_BF16>, dim3(qblocks), dim3(QD_THREADS), 0, s, x, R, K, ncaps, cap0,
+                     cap1, scale_div, fg, amax, out->codes, out->sf, out->scale32, err);
+    else
+      e = launch_pdl(quant_fwd_direct_kernel<Q2_F32>, dim3(qblocks), dim3(QD_THREADS), 0, s, x, R, K, ncaps, cap0,
+                     cap1, scale_div, fg, amax, out->codes, out->sf, out->scale32, err);
+  } else if (dtype == Q2_BF16)
     e = launch_pdl(quant_fwd_kernel<Q2_BF16>, dim3(blocks), dim3(QT + 32), smem, s, x, R, K, ncaps, cap0, cap1,
                    scale_div, fg, amax, out->codes, out->sf, out->scale32, err);
   else
