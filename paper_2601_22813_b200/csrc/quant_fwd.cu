@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
 // groups it still cannot certify the literal float64 restatement
 // (quant_group_exact).  No shared-memory ring, no block barriers, no fix-up lists.
 #ifndef Q2_QDMINB
-#define Q2_QDMINB 3
+#define Q2_QDMINB 4
 #endif
 constexpr int QD_THREADS = 256;
 
@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
     FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
     float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
   __shared__ float mids[128];
+  __shared__ uint32_t pend_all[QD_THREADS / 32][64];        // per-warp list of groups the fast path left undecided
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
@@ -624,32 +625,27 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
   // slot s covers groups [padded - (s + 1) nth, padded - s nth); gid = that base + tid, so
   // gid = tid (mod 32) and lanes 4m..4m+3 hold four consecutive groups
   int64_t gid = padded - nth + (int64_t)blockIdx.x * QD_THREADS + threadIdx.x;
-  uint32_t wn[16];
-  load_group<DT>(x, gid, gid >= 0 && gid < total, wn);
+  uint32_t* const pend = pend_all[threadIdx.x >> 5];
+  uint32_t npend = 0;                                       // warp-uniform
+  auto resolve = [&](uint32_t g) {
+    quant_resolve<DT>(x, g, fast_ok, qc, mids, scale32, ncaps, cap0, cap1, fgpr, gpr, kpr, codes, sf, err);
+  };
   for (; gid > -nth; gid -= nth) {
     const bool live = gid >= 0 && gid < total;
     uint32_t w[16];
-#pragma unroll
-    for (int i = 0; i < (DT == Q2_BF16 ? 8 : 16); ++i) w[i] = wn[i];
-    const int64_t nxt = gid - nth;
-    load_group<DT>(x, nxt, nxt >= 0 && nxt < total, wn);
+    load_group<DT>(x, gid, live, w);
     uint32_t lo = 0, hi = 0, s8 = 0;
+    bool fix = false;
     if (live && amax != 0.f) {
       uint64_t vv[8];
       const float gmax = unpack_group<DT>(w, vv);
       // an all-zero group (or tensor, quantizers.py:219-220): codes 0, scale 0, both errors 0
       if (!(gmax == 0.f && fast_ok)) {
-        auto elem = [&](int k) {
-          return DT == Q2_BF16 ? bf16_to_f32(__ldg(static_cast<const uint16_t*>(x) + gid * GROUP + k))
-                               : __ldg(static_cast<const float*>(x) + gid * GROUP + k);
-        };
-        if (!(fast_ok && group_certified<true>(vv, gmax, qc, mids, elem, lo, hi, s8))) {
-          const uint3 e = quant_group_exact<DT>(x, gid * GROUP, scale32, ncaps, cap0, cap1, err);
-          lo = e.x; hi = e.y; s8 = e.z;
-        }
+        auto no_elem = [&](int) { return 0.f; };
+        fix = !(fast_ok && group_certified<false>(vv, gmax, qc, mids, no_elem, lo, hi, s8));
       }
     }
-    if (live) *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
+    if (live && !fix) *reinterpret_cast<uint2*>(codes + gid * 8) = make_uint2(lo, hi);
     if (quad) {
       // lane 4m stores the scales of groups gid .. gid + 3 (same row, j = 0 mod 4)
       uint32_t wq = s8 << (8 * (lane & 3));
@@ -659,11 +655,26 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
         const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
         *reinterpret_cast<uint32_t*>(sf + sf_offset(r, j, kpr)) = wq;
       }
-    } else if (live) {
+    } else if (live && !fix) {
       const uint32_t r = fgpr.div((uint32_t)gid), j = (uint32_t)gid - r * (uint32_t)gpr;
       sf_store(sf, r, j, kpr, (uint8_t)s8);
     }
+    // undecided groups (exact ties, E4M3 midpoints: a few %) queue per warp and are settled
+    // 32 at a time, one per lane (certified path with exact tie resolution, then float64)
+    const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fix);
+    if (fm) {
+      if (fix) pend[npend + __popc(fm & ((1u << lane) - 1u))] = (uint32_t)gid;
+      npend += __popc(fm);
+      if (npend >= 32) {
+        __syncwarp();
+        resolve(pend[npend - 32 + lane]);
+        npend -= 32;
+        __syncwarp();
+      }
+    }
   }
+  __syncwarp();
+  if ((uint32_t)lane < npend) resolve(pend[lane]);
 }
 
 }  // namespace q2
@@ -731,8 +742,8 @@ static int quant_fwd(const void* x, int dtype, int64_t R, int64_t K, int64_t ld,
   }
   const uint32_t* amax = amax_in ? amax_in : amax_ws;
   cudaError_t e;
-  static const int qeng = getenv("Q2_QUANT_DIRECT") ? 1 : 0;   // 1: the direct kernel (A/B timing; slower on small shapes)
-  if (qeng == 1) {
+  static const int qeng = getenv("Q2_QUANT_RING") ? 1 : 0;     // 1: the shared-memory ring kernel (A/B timing)
+  if (qeng == 0) {
     const int64_t gthreads = (groups + 31) & ~int64_t(31);
     const unsigned qblocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((gthreads + QD_THREADS - 1) / QD_THREADS,
                                                                                (int64_t)Q2_QDMINB * nsm));
