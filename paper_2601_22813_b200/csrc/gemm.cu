@@ -279,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t tsf = tmem + trow + SF_COL + SF_SLOT * s;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          if (g.dbg == 1) break;
+          if (g.dbg == 1 || (g.dbg == 2 && sp != 0) || (g.dbg == 3 && sp != (int)(rank * 0) + 0 && sp != 1)) break;
           const uint4 a4 = *reinterpret_cast<const uint4*>(sfa + 512 * kk + (lane >> 3) * 128 + (lane & 7) * 16);
           const uint4 b0 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + (lane & 7) * 16);
           const uint4 b1 = *reinterpret_cast<const uint4*>(sfb + 1024 * kk + (lane >> 3) * 256 + 128 + (lane & 7) * 16);

@@ -2,7 +2,8 @@
 
 import numpy as np
 
-FAMILIES = ("normal", "lognormal_rows", "coarse_grid", "zero_rows", "outliers", "tiny_chunk", "t2", "tie_grid")
+FAMILIES = ("normal", "lognormal_rows", "coarse_grid", "zero_rows", "outliers", "tiny_chunk", "t2", "tie_grid",
+            "signed_zeros")
 
 
 def make(family: str, shape, seed: int = 0, bf16: bool = True) -> np.ndarray:
@@ -31,6 +32,14 @@ def make(family: str, shape, seed: int = 0, bf16: bool = True) -> np.ndarray:
         # rounding thresholds and E4M3 midpoints
         x = np.clip(np.round(x * 64.0) / 64.0, -5.25, 5.25)
         x.flat[0] = 5.25
+    elif family == "signed_zeros":
+        # 60% exact zeros with random signs (-0 included) on a coarse grid: rotated values
+        # that cancel to exactly 0 are common, and the sign of such a zero in the
+        # reference's butterflies depends on input 0 of the chunk (+0 unless it is -0)
+        x = np.round(x * 2.0) / 2.0
+        zero = rng.random((r, k)) < 0.6
+        x = np.where(zero, np.where(rng.random((r, k)) < 0.5, -0.0, 0.0), x)
+        x[::5, ::128] = -0.0
     elif family != "normal":
         raise ValueError(family)
     x = x.astype(np.float32)
