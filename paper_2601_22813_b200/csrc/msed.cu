@@ -183,6 +183,13 @@ static int dispatch_tc(int src, const TcArgs& a, int pow2, cudaStream_t st) {
 static int tc_pass2(const TcOut& o, uint32_t* err, cudaStream_t st) {
   const int64_t quads = o.R * (o.K / 64);
   if (quads >= (1ll << 31)) return Q2_EINVAL;
+  static const bool old = getenv("Q2_PASS2_OLD") != nullptr;   // A/B timing of the per-quad kernel
+  if (!old && (o.R + 255) / 256 < 65535) {
+    const int64_t kb = (o.K + 63) / 64;
+    return launch_pdl(tc_pass2t_kernel, dim3((unsigned)((kb + 3) / 4), (unsigned)((o.R + 255) / 256)), dim3(256), 0, st,
+                      (const uint16_t*)o.aw, (const unsigned long long*)o.red, (uint32_t)o.R, (uint32_t)o.K, o.sf,
+                      o.scale32, err) == cudaSuccess ? Q2_OK : Q2_ECUDA;
+  }
   if (launch_pdl(tc_pass2_kernel, dim3((unsigned)std::max<int64_t>(1, (quads + 255) / 256)), dim3(256), 0, st,
                  (const uint16_t*)o.aw, (const unsigned long long*)o.red, (uint32_t)o.R, (uint32_t)o.K,
                  FastDiv((uint32_t)(o.K / 64)), o.sf, o.scale32, err) != cudaSuccess)

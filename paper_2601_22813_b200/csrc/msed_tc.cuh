@@ -1114,4 +1114,51 @@ __global__ void __launch_bounds__(256) tc_pass2_kernel(const uint16_t* __restric
   *reinterpret_cast<uint32_t*>(sf + sf_offset(r, 4 * jq, sf_kblocks(K))) = word;
 }
 
+
+// Post-hoc pass 2, tiled: one block per (256-row block, 4 K64 blocks).  Thread t reads
+// the 16 SR words of row 256 rb + t (32 contiguous bytes), turns them into E4M3 codes
+// (normal range: one shift-add of the word, aword_code otherwise), places them at their
+// position in the scale layout in shared memory, and the block writes its 4 KiB of
+// scales contiguously (rows past R get scale 0: deterministic padding).
+__device__ __forceinline__ uint32_t aword_code_fast(uint32_t w, int k, bool* ovf) {
+  const int E = (int)(w >> 7) - 256 - k;
+  if ((w >> 7) != 0u && E >= -6 && E < 8) return (w >> 4) + ((w >> 3) & 1u) - ((uint32_t)(249 + k) << 3);
+  return aword_code(w, k, ovf);
+}
+__global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restrict__ aw,
+                                                        const unsigned long long* __restrict__ red, uint32_t R,
+                                                        uint32_t K, uint8_t* __restrict__ sf,
+                                                        float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
+  __shared__ __align__(16) uint32_t tile[4 * 256];
+  pdl_trigger();
+  pdl_wait();
+  const uint64_t pb = red[1];
+  const double pmax = __longlong_as_double((long long)pb);
+  const int E = (int)(pb >> 52) - 1023;
+  const int k = (pb & ((1ull << 52) - 1)) == 0 ? E - 8 : E - 7;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
+  const uint32_t kb = (K + 63) / 64, jb0 = 4 * blockIdx.x, nj = min(4u, kb - jb0);
+  const uint32_t t = threadIdx.x, r = 256 * blockIdx.y + t;
+  // word of row t within a 1 KiB block: byte (L/8)*256 + h*128 + (L%8)*16 + c*4, row = 128h + 32c + L
+  const uint32_t L = t & 31, c = (t >> 5) & 3, h = t >> 7;
+  const uint32_t widx = (L >> 3) * 64 + h * 32 + (L & 7) * 4 + c;
+  bool ovf = false;
+#pragma unroll
+  for (uint32_t q = 0; q < 4; ++q) {
+    if (q >= nj) break;
+    uint32_t word = 0;
+    if (r < R && pmax > 0.0) {
+      const uint2 w2 = *reinterpret_cast<const uint2*>(aw + (uint64_t)r * (K / GROUP) + 4 * (jb0 + q));
+      word = aword_code_fast(w2.x & 0xFFFFu, k, &ovf) | (aword_code_fast(w2.x >> 16, k, &ovf) << 8) |
+             (aword_code_fast(w2.y & 0xFFFFu, k, &ovf) << 16) | (aword_code_fast(w2.y >> 16, k, &ovf) << 24);
+    }
+    tile[256 * q + widx] = word;
+  }
+  if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(sf + (((uint64_t)blockIdx.y * kb + jb0) << 10));
+  const uint4* src = reinterpret_cast<const uint4*>(tile);
+  for (uint32_t i = t; i < nj * 64; i += 256) dst[i] = src[i];
+}
+
 }  // namespace q2
