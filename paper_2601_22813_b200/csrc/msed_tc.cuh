@@ -59,8 +59,9 @@ constexpr int TC_TILE = 32768;                   // 128 x 128 bf16
 constexpr int TC_RAW = 10240;                    // tape raw tile: codes 8 KB + scales 2 KB
 constexpr int TC_NRAW = 3;
 constexpr int TC_META = 4;                       // metadata ring (tile flags)
-constexpr int TC_META_BYTES = 48;                // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask
+constexpr int TC_META_BYTES = 48;                // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask, [9] tile max bits
 constexpr int TC_DEF_CAP = 256;
+constexpr float TC_SQRT_128NS = 45.26f;        // sqrt(128 * 16): beta_a assumes <= 16 small values per chunk
 constexpr int TC_PF = 6;                         // tiles prefetched into L2 ahead of the TMA ring
 // Shared memory: B operands diag(s) H per orientation (32 KB each) | NS stages of main + small (64 KB each) | tape raw ring |
 // metadata ring | deferred list | misc | barriers.  bf16 sources: 3 stages
@@ -627,6 +628,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       if (st == 0) {
         const bool hs = (misc[8] | misc[9] | misc[10] | misc[11]) != 0u;
         metau[0] = (hs ? 1u : 0u) | (nonfin ? 2u : 0u) | (tiny ? 4u : 0u);
+        metau[9] = M;                                            // tile max |x| bits (bf16 / the tape's f16)
         if (nonfin) misc[12] |= 1u;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       const bool mine = DUAL || ((it & 1) == grp);
       mbar_wait_sleep(bar_mfull + 8 * m, (it / TC_META) & 1);
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES);
-      const uint32_t flags = meta[0];
+      const uint32_t flags = meta[0], tmaxb = meta[9];
       // z0: input 0 of this chunk is -0 after the rotation sign.  Only then can an exactly
       // zero output of the reference's butterflies be -0 (every output's left operand chain
       // ends at input 0; a zero from cancellation is +0), i.e. carry code sign 1.
@@ -753,29 +755,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       }
       // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small),
       // L1(small) <= ||H.small||_2 (Parseval; both halves of Y2), plus flush-to-zero slack
+      // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small), and
+      // L1(small) <= ||H.small||_2 (Parseval).  The decisions below take beta_a, the bound for
+      // a chunk with at most TC_NSMALL small values (each below the split threshold thr):
+      // ||H.small||_2 <= sqrt(128 * TC_NSMALL) * thr.  The chunk's own ||Y2||_2 is summed on the
+      // way (the Y2 loads the decisions need anyway) and a chunk whose bound exceeds beta_a is
+      // recomputed by the literal path -- no separate pass over Y2 before the decisions.
       float beta = 0.f;
       if (has_small) {
-        float sa = 0.f, sb = 0.f, sc = 0.f, sd = 0.f;
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          mbar_wait_sleep(bar_tfull + 8 * (2 * b + h), use & 1);
-          tc_fence_after();
-          uint32_t v2[64];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) tmem_ld16(v2 + 16 * c, tb + 128 * h + 64 + 16 * c);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int i = 0; i < 64; i += 4) {
-            sa = fmaf(__uint_as_float(v2[i]), __uint_as_float(v2[i]), sa);
-            sb = fmaf(__uint_as_float(v2[i + 1]), __uint_as_float(v2[i + 1]), sb);
-            sc = fmaf(__uint_as_float(v2[i + 2]), __uint_as_float(v2[i + 2]), sc);
-            sd = fmaf(__uint_as_float(v2[i + 3]), __uint_as_float(v2[i + 3]), sd);
-          }
-        }
-        const float ss = ((sa + sb) + (sc + sd)) * 1.0001f;
-        beta = ss > 0.f ? __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f) : 0.f;
+        const int Eb = TAPE ? (int)(tmaxb >> 10) - 15 - 10 : (int)(tmaxb >> 7) - 127 - 8;   // log2 thr
+        const float thr = __uint_as_float((uint32_t)max(Eb + 127, 1) << 23);
+        beta = __fmul_ru(__fadd_ru(__fmul_ru(thr, TC_SQRT_128NS * 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f);
       }
-      const bool exact_chunk = beta == 0.f && !tiny;          // y64 = fl64(fl64(Y * scale) * c) exactly
+      uint64_t y2ss = 0;                                      // sum of Y2^2 over the chunk (f32x2)
+      const bool exact_chunk = !has_small && !tiny;            // y64 = fl64(fl64(Y * scale) * c) exactly
       // the sign of a zero / tiny value needs |Y| > betaY -- except an exact zero of an exact
       // chunk without z0, which is +0 in the reference (the fma below makes it +0 here as well)
       const bool sign_chk = !exact_chunk || z0;
@@ -804,6 +797,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (gp & 1) release(h);
+            if (has_small) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const uint64_t p2 = pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]));
+                y2ss = ffma2(p2, p2, y2ss);
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               if (has_small) {
@@ -975,6 +975,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         }
       }
       ++use;
+      if (has_small) {                                        // verify beta_a against this chunk's Y2
+        float s0, s1;
+        upk2(y2ss, s0, s1);
+        const float ss = __fadd_ru(s0, s1) * 1.0001f;
+        const float bact = ss > 0.f ? __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f) : 0.f;
+        if (!(bact <= beta)) defer = true;
+      }
       // S = num64 / den64 = C * num / den (num = sum Y^2, den = sum d_g sum |Y| |q|).  Relative
       // bounds: fp32 group sums of positive terms (<= 6 roundings) and the cross-group sums
       // (<= 7), the rounding of Y (2^-24 |Y|) and the small part (|dY| <= betaY, sum |Y| <=
