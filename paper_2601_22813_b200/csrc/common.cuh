@@ -146,6 +146,14 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// Top 20 bits of mix64(z) (= the top 20 bits of the 53-bit uniform draw): the second
+// product only needs its high word, and the final z ^ (z >> 31) leaves bits >= 33 alone.
+__device__ __forceinline__ uint32_t mix64_top20(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  const uint32_t zl = (uint32_t)z, zh = (uint32_t)(z >> 32);
+  return (__umulhi(zl, 0x133111EBu) + zl * 0x94D049BBu + zh * 0x133111EBu) >> 12;
+}
 // The (seed, stream) prefix of _bits, shared by every index of one stream.
 __host__ __device__ __forceinline__ uint64_t prng_head(uint64_t seed, uint64_t stream) {
   return mix64(mix64(seed + GOLDEN) ^ (stream + GOLDEN));

@@ -1013,18 +1013,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           uint32_t aws[8];
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
-            aws[g] = 0u;
+            // branch-free over the eight groups (a zero scale gives word 0)
             const float sv = g & 1 ? s4s[g >> 1].y : s4s[g >> 1].x;
-            if (!(sv > 0.f)) continue;
+            const bool live = sv > 0.f;
             const float v = S * sv;
             const uint32_t bl = __float_as_uint(__fmul_rd(v, 1.f - es)), bh = __float_as_uint(__fmul_ru(v, 1.f + es));
-            const uint64_t u53 = mix64(ohead ^ ((uint64_t)(g0 + g) + GOLDEN)) >> 11;
-            const uint32_t u20 = (uint32_t)(u53 >> 33), lo20 = bl & 0xFFFFFu, hi20 = bh & 0xFFFFFu;
+            const uint32_t u20 = mix64_top20(ohead ^ ((uint64_t)(g0 + g) + GOLDEN)), lo20 = bl & 0xFFFFFu,
+                           hi20 = bh & 0xFFFFFu;
             const bool same = (bl >> 20) == (bh >> 20) && lo20 > 0u && bl >= 0x02000000u && bh < 0x7E000000u;
-            if (!same || (u20 >= lo20 && u20 <= hi20)) srdef = 1u;
+            if (live && (!same || (u20 >= lo20 && u20 <= hi20))) srdef = 1u;
             const uint32_t up = u20 < lo20 ? 1u : 0u;
-            const int E = (int)(bl >> 23) - 127;
-            aws[g] = ((uint32_t)(E + 256) << 7) | (((bl >> 20) & 7u) << 4) | (up << 3);
+            aws[g] = live ? ((bl >> 23) + 129u) << 7 | (((bl >> 20) & 7u) << 4) | (up << 3) : 0u;   // E + 256 = (bl >> 23) + 129
           }
           if (!srdef) {
             if (MODE == TC_POSTHOC) {
