@@ -59,9 +59,9 @@ constexpr int TC_TILE = 32768;                   // 128 x 128 bf16
 constexpr int TC_RAW = 10240;                    // tape raw tile: codes 8 KB + scales 2 KB
 constexpr int TC_NRAW = 3;
 constexpr int TC_META = 4;                       // metadata ring (tile flags)
-constexpr int TC_META_BYTES = 48;                // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask, [9] tile max bits
+constexpr int TC_META_BYTES = 320;               // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask, [9] tile max
+                                                 // bits; bytes 64..191 small count per row chunk, 192..319 per column chunk
 constexpr int TC_DEF_CAP = 256;
-constexpr float TC_SQRT_128NS = 45.26f;        // sqrt(128 * 16): beta_a assumes <= 16 small values per chunk
 constexpr int TC_PF = 6;                         // tiles prefetched into L2 ahead of the TMA ring
 // Shared memory: B operands diag(s) H per orientation (32 KB each) | NS stages of main + small (64 KB each) | tape raw ring |
 // metadata ring | deferred list | misc | barriers.  bf16 sources: 3 stages
@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         const int tr = (int)a.fc.div((uint32_t)t);
         const unsigned char* raw = smem + LY::OFF_RAW + rs * TC_RAW;
         const int kr = st, L = kr & 31;
+        uint32_t scmax = 0u, scmin = 255u;                        // E4M3 scale codes of the row (min over nonzero)
 #pragma unroll 1
         for (int qd = 0; qd < (a.dbg == 6 ? 0 : 4); ++qd) {                       // 32 tape columns per quarter
           const uint4 cw = *reinterpret_cast<const uint4*>(raw + kr * 64 + qd * 16);
@@ -513,6 +514,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             const uint32_t s8 = (sfw >> (8 * (2 * (qd & 1) + g))) & 0xFF;
+            scmax = max(scmax, s8);
+            scmin = min(scmin, s8 ? s8 : 255u);
             asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(sc[g])
                 : "h"((unsigned short)(s8 | (s8 << 8))));
           }
@@ -538,9 +541,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             metau[5 + qd] = (a.o[1].sign[0] & 1u) ? zm : 0u;   // tape zeros are +0: -0 iff s[0] < 0
           }
         }
+        scmax = __reduce_max_sync(0xFFFFFFFFu, scmax);
+        scmin = __reduce_min_sync(0xFFFFFFFFu, scmin);
+        if (lane == 0) misc[8 + sw] = (scmax << 8) | scmin;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_rawe + 8 * rs);
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        // No small values are possible when the tile's nonzero scales span <= 5 binades: every
+        // nonzero value is >= 0.5 E(min) while the split threshold is <= 6 E(max) / 2^10 (E(max) /
+        // E(min) < 64 < 85).  Then the split passes are skipped: main = the decoded tile.
+        uint32_t cmax = 0u, cmin = 255u;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) { cmax = max(cmax, misc[8 + w4] >> 8); cmin = min(cmin, misc[8 + w4] & 255u); }
+        const bool no_small = cmax == 0u || (cmin >= 8u && (cmax >> 3) - (cmin >> 3) <= 5u);
+        asm volatile("bar.sync 1, 128;" ::: "memory");          // misc[8..11] is reused by pass 1
+        if (no_small && a.dbg < 2) {
+          if (st == 0) { metau[0] = 0u; metau[9] = 0u; }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (lane == 0) { mbar_arrive(bar_split + 8 * s); mbar_arrive(bar_mfull + 8 * m); }
+          continue;
+        }
       }
       if (a.dbg >= 2) {
         if (st == 0) metau[0] = 1u;
@@ -575,6 +596,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
       if (lane == 0) misc[8 + sw] = mx;
       if (!TAPE && st < 8) metau[1 + st] = 0u;
+      if (st < 32) metau[48 + st] = 0u;                          // column small counts (atomic byte sums)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (!TAPE) {
         // rows: thread st (piece 0) saw rows st/8 + 16 i at bit i; cols: thread st < 8 saw columns
@@ -597,8 +619,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       constexpr int SPLIT = TAPE ? 10 : 8;
       const uint32_t thr = Ef >= SPLIT + 1 ? (uint32_t)(Ef - SPLIT) << (TAPE ? 10 : 7) : 0u;
       const uint32_t thr2 = thr | (thr << 16);
-      // pass 2: main/small split (the absmax pass rotates the raw tile: no split)
-      uint32_t anys = 0;
+      // pass 2: main/small split (the absmax pass rotates the raw tile: no split), and the
+      // number of nonzero small values of every row and column chunk (byte counters: the
+      // flag bytes of four elements at a time)
+      uint32_t anys = 0, rc[8], cc[2][2] = {{0u, 0u}, {0u, 0u}};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rc[j] = 0u;
 #pragma unroll
       for (int i = 0; i < (MODE == TC_ABSMAX ? 0 : 16); ++i) {
         const int p = st + 128 * i, sl = p >> 10, row = (p & 1023) >> 3;
@@ -620,6 +646,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         }
         *reinterpret_cast<uint4*>(mainp + off) = make_uint4(mo[0], mo[1], mo[2], mo[3]);
         *reinterpret_cast<uint4*>(smallp + off) = make_uint4(so[0], so[1], so[2], so[3]);
+        uint32_t t4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t4[e] = ((so[e] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;   // nonzero small
+        uint32_t fa, fb;                                         // flag bytes of elements 0-3 / 4-7
+        asm("prmt.b32 %0, %1, %2, 0x7531;" : "=r"(fa) : "r"(t4[0]), "r"(t4[1]));
+        asm("prmt.b32 %0, %1, %2, 0x7531;" : "=r"(fb) : "r"(t4[2]), "r"(t4[3]));
+        fa = (fa >> 7) & 0x01010101u;
+        fb = (fb >> 7) & 0x01010101u;
+        rc[i & 7] += __popc(fa | (fb << 1));
+        cc[i >> 3][0] += fa;
+        cc[i >> 3][1] += fb;
+      }
+      if (MODE != TC_ABSMAX) {
+        // rows st/8 + 16 j: the eight lanes 8k..8k+7 hold their pieces
+        uint8_t* const rcnt = reinterpret_cast<uint8_t*>(metau + 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t v = rc[j];
+          v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+          v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+          v += __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+          if (piece == 0) rcnt[st / 8 + 16 * j] = (uint8_t)v;
+        }
+        // columns 64 sl + 8 piece + e: lanes piece + 8 m of the four warps (byte sums <= 128)
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2) {
+            uint32_t v = cc[a2][b2];
+            v += __shfl_xor_sync(0xFFFFFFFFu, v, 8);
+            v += __shfl_xor_sync(0xFFFFFFFFu, v, 16);
+            if (lane < 8 && v) atomicAdd(&metau[48 + (a2 * 8 + piece) * 2 + b2], v);
+          }
       }
       const bool anyw = __any_sync(0xFFFFFFFFu, (anys & 0x7FFF7FFFu) != 0u);
       if (lane == 0) misc[8 + sw] = anyw ? 1u : 0u;
@@ -698,6 +757,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       mbar_wait_sleep(bar_mfull + 8 * m, (it / TC_META) & 1);
       const uint32_t* meta = reinterpret_cast<const uint32_t*>(smem + LY::OFF_META + m * TC_META_BYTES);
       const uint32_t flags = meta[0], tmaxb = meta[9];
+      const uint32_t nsmall = reinterpret_cast<const uint8_t*>(meta + 16)[(o ? 128 : 0) + rt];   // small values in the chunk
       // z0: input 0 of this chunk is -0 after the rotation sign.  Only then can an exactly
       // zero output of the reference's butterflies be -0 (every output's left operand chain
       // ends at input 0; a zero from cancellation is +0), i.e. carry code sign 1.
@@ -755,20 +815,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       }
       // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small),
       // L1(small) <= ||H.small||_2 (Parseval; both halves of Y2), plus flush-to-zero slack
-      // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small), and
-      // L1(small) <= ||H.small||_2 (Parseval).  The decisions below take beta_a, the bound for
-      // a chunk with at most TC_NSMALL small values (each below the split threshold thr):
-      // ||H.small||_2 <= sqrt(128 * TC_NSMALL) * thr.  The chunk's own ||Y2||_2 is summed on the
-      // way (the Y2 loads the decisions need anyway) and a chunk whose bound exceeds beta_a is
-      // recomputed by the literal path -- no separate pass over Y2 before the decisions.
+      // beta: bound (y units) of |Y2 - H.small| over the chunk: 32 * 2^-24 * L1(small), with
+      // L1(small) <= n * thr (the split warps counted the chunk's n small values, each below
+      // the split threshold thr), plus flush-to-zero slack.  A chunk without small values is
+      // exact.
       float beta = 0.f;
-      if (has_small) {
+      if (has_small && nsmall != 0u) {
         const int Eb = TAPE ? (int)(tmaxb >> 10) - 15 - 10 : (int)(tmaxb >> 7) - 127 - 8;   // log2 thr
         const float thr = __uint_as_float((uint32_t)max(Eb + 127, 1) << 23);
-        beta = __fmul_ru(__fadd_ru(__fmul_ru(thr, TC_SQRT_128NS * 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f);
+        beta = __fmul_ru(__fadd_ru(__fmul_ru(thr * (float)nsmall, 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f);
       }
-      uint64_t y2ss = 0;                                      // sum of Y2^2 over the chunk (f32x2)
-      const bool exact_chunk = !has_small && !tiny;            // y64 = fl64(fl64(Y * scale) * c) exactly
+      const bool exact_chunk = beta == 0.f && !tiny;          // y64 = fl64(fl64(Y * scale) * c) exactly
       // the sign of a zero / tiny value needs |Y| > betaY -- except an exact zero of an exact
       // chunk without z0, which is +0 in the reference (the fma below makes it +0 here as well)
       const bool sign_chk = !exact_chunk || z0;
@@ -797,13 +854,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (gp & 1) release(h);
-            if (has_small) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const uint64_t p2 = pk2(__uint_as_float(v2[i]), __uint_as_float(v2[i + 1]));
-                y2ss = ffma2(p2, p2, y2ss);
-              }
-            }
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               if (has_small) {
@@ -975,13 +1025,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         }
       }
       ++use;
-      if (has_small) {                                        // verify beta_a against this chunk's Y2
-        float s0, s1;
-        upk2(y2ss, s0, s1);
-        const float ss = __fadd_ru(s0, s1) * 1.0001f;
-        const float bact = ss > 0.f ? __fmul_ru(__fadd_ru(__fmul_ru(__fsqrt_ru(ss), 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f) : 0.f;
-        if (!(bact <= beta)) defer = true;
-      }
       // S = num64 / den64 = C * num / den (num = sum Y^2, den = sum d_g sum |Y| |q|).  Relative
       // bounds: fp32 group sums of positive terms (<= 6 roundings) and the cross-group sums
       // (<= 7), the rounding of Y (2^-24 |Y|) and the small part (|dY| <= betaY, sum |Y| <=
