@@ -72,6 +72,7 @@ struct GemmArgs {
   int tiles_m, tiles_n, nk;
   int accumulate;
   int dbg;                                                // timing probes: 1 = scale warps skip their TMEM writes
+  int sfcp;                                               // 1: the MMA thread copies scales to TMEM (tcgen05.cp), no scale warps
   unsigned long long* trace;                              // optional timeline probe (pair 0), else nullptr
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -215,6 +216,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
           const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s, sb = bar_sff + 8 * s;
+          if (g.sfcp) {
+            // scales of both CTAs complete on the leader's full barrier with the operands
+            if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST + SFA_ST + SFB_ST));
+            tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
+            tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
+            tma2_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, fb);
+            tma2_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, fb);
+            continue;
+          }
           if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST));
           tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
           tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
@@ -238,13 +248,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           const unsigned long long t0 = g.trace ? gtime() : 0;
           mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
           const unsigned long long t1 = g.trace ? gtime() : 0;
-          mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
+          if (!g.sfcp) mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
           if (g.trace) { wf += t1 - t0; ws += gtime() - t1; }
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE);
           const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_ST);
           const uint32_t tsf = tmem + SF_COL + SF_SLOT * s;
           const int nsub = min(4, g.K / 64 - 4 * kt);          // K tail: no MMA past K
+          if (g.sfcp) {
+            // scales of this stage into its own TMEM slot (distinct per stage and K64 block, so
+            // the copies never wait on an MMA still reading the previous contents); the tensor
+            // pipe runs them in issue order ahead of the MMAs that read them.  32x128b.warpx4
+            // replicates each 512 B half to the four subpartitions.
+            const uint32_t sfa = st + A_ST + B_ST, sfb = sfa + SFA_ST;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk >= nsub) break;
+              tc2_cp_sf(tsf + 12 * kk, desc_sf32(sfa + 512 * kk, 128));
+              tc2_cp_sf(tsf + 12 * kk + 4, desc_sf32(sfb + 1024 * kk, 256));
+              tc2_cp_sf(tsf + 12 * kk + 8, desc_sf32(sfb + 1024 * kk + 128, 256));
+            }
+          }
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             if (kk >= nsub) break;
@@ -256,7 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         if (g.trace && pair == 0 && tc < 64) { g.trace[4 * tc + 1] = gtime(); g.trace[256 + 2 * tc] = wf; g.trace[257 + 2 * tc] = ws; }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 8 && !g.sfcp) {
     // ---------------- scale warps: raw scales -> TMEM (both CTAs) ----------------
     // Warp 4+sp writes TMEM lanes 32sp..32sp+31, i.e. one replica of every
     // scale vector; lane L holds rows 32c + L (c = column within a 4-group).
@@ -457,8 +481,11 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
     return Q2_ECUDA;
   static unsigned long long* trace = nullptr;
   if (getenv("Q2_GEMM_TRACE") && !trace) cudaMalloc(&trace, 64 * 8 * 8);
+  // A/B option: scales copied by the MMA thread with tcgen05.cp (measured 1.3-1.7x slower: each
+  // 512-byte 32x128b.warpx4 copy holds the tensor pipe ~60 cycles, 12 per stage > the stage's MMAs)
+  static const int g_gemm_cp = getenv("Q2_GEMM_CP") ? atoi(getenv("Q2_GEMM_CP")) : 0;
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
-             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_DBG") ? atoi(getenv("Q2_GEMM_DBG")) : 0,
+             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_DBG") ? atoi(getenv("Q2_GEMM_DBG")) : 0, g_gemm_cp,
              getenv("Q2_GEMM_TRACE") ? trace : nullptr};
   if (g.trace) cudaMemsetAsync(trace, 0, 64 * 8 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
