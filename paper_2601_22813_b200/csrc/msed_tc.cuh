@@ -311,6 +311,13 @@ __device__ __forceinline__ double tc_scale32(const TcOut& o, double s, int pow2)
   return ldexp(1.0, (m == 0.5) ? e - 1 : e);
 }
 
+// E4M3 code of an SR word: normal range by one shift-add of the word, aword_code otherwise
+__device__ __forceinline__ uint32_t aword_code_fast(uint32_t w, int k, bool* ovf) {
+  const int E = (int)(w >> 7) - 256 - k;
+  if ((w >> 7) != 0u && E >= -6 && E < 8) return (w >> 4) + ((w >> 3) & 1u) - ((uint32_t)(249 + k) << 3);
+  return aword_code(w, k, ovf);
+}
+
 template <int SRC, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ TcArgs a,
                                                                  int pow2) {
@@ -721,6 +728,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     const float invC = __frcp_ru(C) * 1.0001f;                          // upper bound of 1/C
     const float is_lo = __frcp_rd((float)a.s), is_hi = __frcp_ru((float)a.s); // brackets of 1/s
     const double qs = MODE == TC_QUANT ? qscale[o] : 0.0;
+    const float qsf = (float)qs;                              // scale32 is a float value: exact
     const float isd_lo = qs > 0.0 ? __double2float_rd(__drcp_rd(__dmul_rn(qs, a.s))) : 0.f;
     const float isd_hi = qs > 0.0 ? __double2float_ru(__drcp_ru(__dmul_rn(qs, a.s))) : 0.f;
     auto push_deferred = [&](bool want, int t) {            // warp-collective
@@ -808,7 +816,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
         const float yv = ym * C, ee = __fmaf_ru(yv, 0x1p-21f, bt);
         const float yu = __fadd_ru(yv, ee), yl = fmaxf(__fsub_rd(yv, ee), 0.f);
         atomicMax(misc + 4 + o, __float_as_uint(yl));
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");   // the tile's lower bounds are in
+        // no barrier: Lrun may miss this tile's lower bounds (any value <= the true max is a valid
+        // threshold; a stale one only sends a few more chunks to the literal path)
         const float Lrun = __uint_as_float(misc[4 + o]);
         push_deferred(tiny || yu >= Lrun, t);
         continue;
@@ -917,14 +926,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
               const bool live = qs != 0.0 && gm != 0.f;
               unc |= live && (cl != ch || !(isd_hi < 0x1p120f));
               s4 = live ? (float)e4m3_val(cl) : 0.f;
-              d64 = __dmul_rn((double)s4, qs);
-              d = (float)d64;                                   // rounded: inside the code margin
+              // E4M3 (4 significant bits) x scale32 (a float) is exact in double, so its float
+              // rounding is one fp32 product; the double value is only needed by the fix path
+              d = __fmul_rn(s4, qsf);                           // rounded: inside the code margin
             }
             // the sign of a zero / tiny value: |Y| > betaY (see sign_chk)
             unc |= sign_chk && !(mnv[gq] > betaY);
             s4v[gq] = s4;
             dv[gq] = d;
-            d64v[gq] = MODE == TC_POSTHOC ? (double)d : d64;
+            d64v[gq] = MODE == TC_POSTHOC ? (double)d : (double)s4 * (double)qsf;   // exact
             uncv[gq] = unc;
             dokv[gq] = d > 0.f && !unc;
           }
@@ -1016,7 +1026,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             if (uncv[gq]) defer = true;
             nh += numv[gq];
             const float s4 = s4v[gq];
-            dh = fmaf(denv[gq], s4 > 0.f ? (MODE == TC_POSTHOC ? s4 : (float)__dmul_rn((double)s4, qs)) : 0.f, dh);
+            dh = fmaf(denv[gq], MODE == TC_POSTHOC ? s4 : dv[gq], dh);   // s4 = 0 gives d = 0
           }
           s4s[gp] = make_float2(s4v[0], s4v[1]);
           // codes of the two groups: 16 bytes
@@ -1077,8 +1087,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
                 bool o2 = false, o3 = false;
-                w0 |= aword_code(aws[g], 0, &o2) << (8 * g);
-                w1 |= aword_code(aws[g + 4], 0, &o3) << (8 * g);
+                w0 |= aword_code_fast(aws[g], 0, &o2) << (8 * g);
+                w1 |= aword_code_fast(aws[g + 4], 0, &o3) << (8 * g);
                 if (o2 || o3) ovf = true;
               }
               *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8, okb)) = w0;
@@ -1169,11 +1179,6 @@ __global__ void __launch_bounds__(256) tc_pass2_kernel(const uint16_t* __restric
 // (normal range: one shift-add of the word, aword_code otherwise), places them at their
 // position in the scale layout in shared memory, and the block writes its 4 KiB of
 // scales contiguously (rows past R get scale 0: deterministic padding).
-__device__ __forceinline__ uint32_t aword_code_fast(uint32_t w, int k, bool* ovf) {
-  const int E = (int)(w >> 7) - 256 - k;
-  if ((w >> 7) != 0u && E >= -6 && E < 8) return (w >> 4) + ((w >> 3) & 1u) - ((uint32_t)(249 + k) << 3);
-  return aword_code(w, k, ovf);
-}
 __global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restrict__ aw,
                                                         const unsigned long long* __restrict__ red, uint32_t R,
                                                         uint32_t K, uint8_t* __restrict__ sf,
