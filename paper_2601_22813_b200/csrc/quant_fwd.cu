@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
 #define Q2_QDMINB 4
 #endif
 constexpr int QD_THREADS = 256;
+constexpr int QD_CAP = 256;                               // per-warp queue of undecided groups
 
 template <int DT>
 __device__ __forceinline__ void load_group(const void* x, int64_t gid, bool live, uint32_t (&w)[16]) {
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
     FastDiv fgpr, const uint32_t* __restrict__ amax_bits, uint8_t* __restrict__ codes, uint8_t* __restrict__ sf,
     float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
   __shared__ float mids[128];
-  __shared__ uint32_t pend_all[QD_THREADS / 32][64];        // per-warp list of groups the fast path left undecided
+  __shared__ uint32_t pend_all[QD_THREADS / 32][QD_CAP];    // per-warp list of groups the fast path left undecided
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x < 127) mids[threadIdx.x] = threadIdx.x < 126 ? 0.5f * (e4m3_valf(threadIdx.x) + e4m3_valf(threadIdx.x + 1)) : __int_as_float(0x7f800000);
@@ -630,7 +631,12 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
   auto resolve = [&](uint32_t g) {
     quant_resolve<DT>(x, g, fast_ok, qc, mids, scale32, ncaps, cap0, cap1, fgpr, gpr, kpr, codes, sf, err);
   };
-  for (; gid > -nth; gid -= nth) {
+  // The streaming loop has no call in it (the resolve path's calling convention cost spills
+  // on every iteration); it leaves when the queue is nearly full, which drains it 32 at a time.
+  // loop bounds on the warp's first group (gid - lane): every lane runs the same iterations
+  // (the ballots below need the full warp); lanes past either end are simply not live
+  for (;;) {
+  for (; gid - lane > -nth - 31; gid -= nth) {
     const bool live = gid >= 0 && gid < total;
     uint32_t w[16];
     load_group<DT>(x, gid, live, w);
@@ -665,15 +671,17 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
     if (fm) {
       if (fix) pend[npend + __popc(fm & ((1u << lane) - 1u))] = (uint32_t)gid;
       npend += __popc(fm);
-      if (npend >= 32) {
-        __syncwarp();
-        resolve(pend[npend - 32 + lane]);
-        npend -= 32;
-        __syncwarp();
-      }
+      if (npend > QD_CAP - 32) { gid -= nth; break; }
     }
   }
   __syncwarp();
+  while (npend >= 32) {
+    resolve(pend[npend - 32 + lane]);
+    npend -= 32;
+    __syncwarp();
+  }
+  if (gid - lane <= -nth - 31) break;
+  }
   if ((uint32_t)lane < npend) resolve(pend[lane]);
 }
 
