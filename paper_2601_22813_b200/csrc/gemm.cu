@@ -72,7 +72,8 @@ struct GemmArgs {
   int tiles_m, tiles_n, nk;
   int accumulate;
   int dbg;                                                // timing probes: 1 = scale warps skip their TMEM writes
-  int sfcp;                                               // 1: the MMA thread copies scales to TMEM (tcgen05.cp), no scale warps
+  int sfcp;                                               // 1: the MMA thread copies all scales (tcgen05.cp), no scale warps
+  int cpmask;                                             // sfcp == 0: bit s = stage s's scales by the copier thread
   unsigned long long* trace;                              // optional timeline probe (pair 0), else nullptr
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -180,7 +181,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_sff + 8 * s, 1);
-      mbar_init(bar_sfr + 8 * s, 8);                          // 4 scale warps x 2 CTAs
+      mbar_init(bar_sfr + 8 * s, (g.cpmask >> s) & 1 ? 1 : 8);  // copier commit / 4 scale warps x 2 CTAs
       mbar_init(bar_empty + 8 * s, 1);
     }
     mbar_init(bar_accf, 1);
@@ -216,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
           const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s, sb = bar_sff + 8 * s;
-          if (g.sfcp) {
+          if (g.sfcp || ((g.cpmask >> s) & 1)) {
             // scales of both CTAs complete on the leader's full barrier with the operands
             if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST + SFA_ST + SFB_ST));
             tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
@@ -280,7 +281,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         if (g.trace && pair == 0 && tc < 64) { g.trace[4 * tc + 1] = gtime(); g.trace[256 + 2 * tc] = wf; g.trace[257 + 2 * tc] = ws; }
       }
     }
-  } else if (warp >= 4 && warp < 8 && !g.sfcp) {
+  } else if (warp == 3 && g.cpmask) {
+    // ---------------- scale copier (leader, one thread): tcgen05.cp of the masked stages'
+    // scales into their TMEM slots, off the MMA thread; a commit signals the MMA thread.
+    // The copies cost tensor-pipe time (~60 cycles per 512 B) but no shared-memory reads
+    // beyond the 6 KB of the stage, so splitting stages between this thread and the scale
+    // warps balances the pipe against shared-memory bandwidth; with few K stages per tile
+    // the copier runs ahead while the MMA waits for the accumulator drain.
+    if (rank == 0 && lane == 0) {
+      const int my_tiles = pair < ntiles ? (ntiles - 1 - pair) / npairs + 1 : 0;
+      const int total = my_tiles * g.nk;
+      for (int it = 0; it < total; ++it) {
+        const int s = it % STAGES, kt = it % g.nk;
+        if (!((g.cpmask >> s) & 1)) continue;
+        mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * STAGE), sfa = st + A_ST + B_ST, sfb = sfa + SFA_ST;
+        const uint32_t tsf = tmem + SF_COL + SF_SLOT * s;
+        const int nsub = min(4, g.K / 64 - 4 * kt);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          if (kk >= nsub) break;
+          tc2_cp_sf(tsf + 12 * kk, desc_sf32(sfa + 512 * kk, 128));
+          tc2_cp_sf(tsf + 12 * kk + 4, desc_sf32(sfb + 1024 * kk, 256));
+          tc2_cp_sf(tsf + 12 * kk + 8, desc_sf32(sfb + 1024 * kk + 128, 256));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     ::"r"(bar_sfr + 8 * s), "h"((unsigned short)1) : "memory");
+      }
+    }
+  } else if (warp >= 4 && warp < 8 && !g.sfcp && g.cpmask != (1 << STAGES) - 1) {
     // ---------------- scale warps: raw scales -> TMEM (both CTAs) ----------------
     // Warp 4+sp writes TMEM lanes 32sp..32sp+31, i.e. one replica of every
     // scale vector; lane L holds rows 32c + L (c = column within a 4-group).
@@ -297,6 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       for (int u = 0; u < Q2_SF_BATCH; ++u) {
         if (u >= nb) break;
         const int s = (it + u) % STAGES;
+        if ((g.cpmask >> s) & 1) continue;                    // the copier's stage
         mbar_wait_sleep(bar_sff + 8 * s, ((it + u) / STAGES) & 1);
         const unsigned char* sfa = smem + s * STAGE + A_ST + B_ST;
         const unsigned char* sfb = sfa + SFA_ST;
@@ -318,7 +349,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0)
-        for (int u = 0; u < nb; ++u) mbar_arrive_leader(bar_sfr + 8 * ((it + u) % STAGES));
+        for (int u = 0; u < nb; ++u)
+          if (!((g.cpmask >> ((it + u) % STAGES)) & 1)) mbar_arrive_leader(bar_sfr + 8 * ((it + u) % STAGES));
     }
   } else if (warp >= 8) {
     // ---------------- epilogue ----------------
@@ -484,8 +516,14 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
   // A/B option: scales copied by the MMA thread with tcgen05.cp (measured 1.3-1.7x slower: each
   // 512-byte 32x128b.warpx4 copy holds the tensor pipe ~60 cycles, 12 per stage > the stage's MMAs)
   static const int g_gemm_cp = getenv("Q2_GEMM_CP") ? atoi(getenv("Q2_GEMM_CP")) : 0;
+  // stages whose scales the copier thread moves: all of them for short K (<= 12 stages of
+  // 256 per tile: the copier runs ahead during the accumulator drain), a share for long K
+  static const int g_mask_long = getenv("Q2_GEMM_CPMASK_LONG") ? (int)strtol(getenv("Q2_GEMM_CPMASK_LONG"), nullptr, 0) : 0x15;
+  static const int g_mask_short = getenv("Q2_GEMM_CPMASK_SHORT") ? (int)strtol(getenv("Q2_GEMM_CPMASK_SHORT"), nullptr, 0) : 0x1F;
+  const int nk_tiles = (int)((a->K / 2 + BKB - 1) / BKB);
+  const int cpmask = g_gemm_cp ? 0 : (nk_tiles <= 12 ? g_mask_short : g_mask_long);
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
-             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_DBG") ? atoi(getenv("Q2_GEMM_DBG")) : 0, g_gemm_cp,
+             (int)((a->R + PT - 1) / PT), (int)((b->R + PT - 1) / PT), (int)((a->K / 2 + BKB - 1) / BKB), accumulate, getenv("Q2_GEMM_DBG") ? atoi(getenv("Q2_GEMM_DBG")) : 0, g_gemm_cp, cpmask,
              getenv("Q2_GEMM_TRACE") ? trace : nullptr};
   if (g.trace) cudaMemsetAsync(trace, 0, 64 * 8 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
