@@ -47,7 +47,8 @@ constexpr int SFA_ST = 2048;                              // 4 K64 blocks x the 
 constexpr int SFB_ST = 4096;                              // 4 K64 blocks x both halves
 constexpr int STAGE = A_ST + B_ST + SFA_ST + SFB_ST;      // 38 KB
 constexpr int STAGES = 5;
-constexpr int OFF_BAR = STAGES * STAGE;
+constexpr int OFF_EPI = STAGES * STAGE;                   // bf16 epilogue staging: 4 KB per epilogue warp
+constexpr int OFF_BAR = OFF_EPI + 8 * 4096;
 constexpr int GEMM_SMEM = OFF_BAR + 256 + 1024;
 constexpr int GEMM_THREADS = 512;
 constexpr int TMEM_COLS = 512;
@@ -56,6 +57,9 @@ constexpr int SF_COL = 256, SF_SLOT = 48;                 // per stage: 4 x (SFA
 #define Q2_GROUP_M 8
 #endif
 constexpr int GROUP_M = Q2_GROUP_M;
+#ifndef Q2_GEMM_STAGE_EPI
+#define Q2_GEMM_STAGE_EPI 1
+#endif
 #ifndef Q2_SF_BATCH
 #define Q2_SF_BATCH 2
 #endif
@@ -385,8 +389,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(bar_acce);          // MMA may overwrite the accumulator
         if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
-        if (gm >= g.M) continue;
         __nv_bfloat16* dr = reinterpret_cast<__nv_bfloat16*>(drow);
+        if (Q2_GEMM_STAGE_EPI && tm * PT + (int)rank * 128 + 128 <= g.M && gn0 + 128 <= g.N) {
+          // coalesced stores: the warp's 32 rows x 64 columns go through 4 KB of shared memory
+          // (16-byte chunks swizzled by row) and leave as 4 full 128-byte row segments per
+          // store instruction instead of 32 partial ones
+          unsigned char* stg = smem + OFF_EPI + 4096 * e;
+          const int lr = lane >> 3, lc = lane & 7;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              uint32_t p[4];
+              if (hh == 0) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) p[i] = pk[4 * c + i];
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int j = 8 * c + 2 * i;
+                  __nv_bfloat162 h = __floats2bfloat162_rn(alpha * __uint_as_float(v[j]), alpha * __uint_as_float(v[j + 1]));
+                  p[i] = *reinterpret_cast<uint32_t*>(&h);
+                }
+              }
+              *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+            }
+            __syncwarp();
+            const int64_t row0 = (int64_t)(tm * PT + (int)rank * 128 + sp * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + lr;
+              const uint4 q = *reinterpret_cast<const uint4*>(stg + r * 128 + ((lc ^ (r & 7)) << 4));
+              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.d) + (row0 + r) * g.ldd + gn0 + 64 * hh + 8 * lc) = q;
+            }
+            __syncwarp();
+          }
+          continue;
+        }
+        if (gm >= g.M) continue;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {                        // 8 columns per 16-byte store
           uint32_t p[4];
@@ -420,6 +460,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(bar_acce);        // MMA may overwrite the accumulator
           if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
+        }
+        if (F32 && Q2_GEMM_STAGE_EPI && tm * PT + (int)rank * 128 + 128 <= g.M && gn0 + 128 <= g.N) {
+          // coalesced fp32 stores (and accumulate reads) through the warp's 4 KB of shared memory
+          unsigned char* stg = smem + OFF_EPI + 4096 * e;
+          const int lr = lane >> 3, lc = lane & 7;
+          const int64_t row0 = (int64_t)(tm * PT + (int)rank * 128 + sp * 32);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_float4(alpha * __uint_as_float(v[q][4 * c]), alpha * __uint_as_float(v[q][4 * c + 1]),
+                              alpha * __uint_as_float(v[q][4 * c + 2]), alpha * __uint_as_float(v[q][4 * c + 3]));
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + lr;
+              float4 o = *reinterpret_cast<const float4*>(stg + r * 128 + ((lc ^ (r & 7)) << 4));
+              float* dp = static_cast<float*>(g.d) + (row0 + r) * g.ldd + gn0 + 64 * half + 32 * q + 4 * lc;
+              if (g.accumulate) { const float4 pv = *reinterpret_cast<const float4*>(dp); o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w; }
+              *reinterpret_cast<float4*>(dp) = o;
+            }
+            __syncwarp();
+          }
+          continue;
         }
         if (gm >= g.M) continue;
 #pragma unroll
