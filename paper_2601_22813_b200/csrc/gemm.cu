@@ -581,10 +581,11 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
   // A/B option: scales copied by the MMA thread with tcgen05.cp (measured 1.3-1.7x slower: each
   // 512-byte 32x128b.warpx4 copy holds the tensor pipe ~60 cycles, 12 per stage > the stage's MMAs)
   static const int g_gemm_cp = getenv("Q2_GEMM_CP") ? atoi(getenv("Q2_GEMM_CP")) : 0;
-  // stages whose scales the copier thread moves: all of them for short K (<= 12 stages of
-  // 256 per tile: the copier runs ahead during the accumulator drain), a share for long K
+  // stages whose scales the copier thread moves (the rest by the scale warps): three of five
+  // measured best for short (<= 12 stages of 256 per tile) and long K alike once the epilogue
+  // stores were staged (sweeps of 0x0A..0x1F, tools/gemm_c3.py); kept as two knobs
   static const int g_mask_long = getenv("Q2_GEMM_CPMASK_LONG") ? (int)strtol(getenv("Q2_GEMM_CPMASK_LONG"), nullptr, 0) : 0x15;
-  static const int g_mask_short = getenv("Q2_GEMM_CPMASK_SHORT") ? (int)strtol(getenv("Q2_GEMM_CPMASK_SHORT"), nullptr, 0) : 0x1F;
+  static const int g_mask_short = getenv("Q2_GEMM_CPMASK_SHORT") ? (int)strtol(getenv("Q2_GEMM_CPMASK_SHORT"), nullptr, 0) : 0x15;
   const int nk_tiles = (int)((a->K / 2 + BKB - 1) / BKB);
   const int cpmask = g_gemm_cp ? 0 : (nk_tiles <= 12 ? g_mask_short : g_mask_long);
   GemmArgs g{a->scale32, b->scale32, d, ldd, (int)a->R, (int)b->R, (int)a->K, (int)sf_kblocks(a->K),
