@@ -55,6 +55,14 @@ __host__ __device__ __forceinline__ double e4m3_val(uint32_t code) {
   return (double)(8 + m) * ldexp(1.0, (int)e - 10);
 #endif
 }
+// The same value as a float (exact): code < 8 is k * 2^-9, else (8 + m) 2^(e-10).
+__host__ __device__ __forceinline__ float e4m3_valf(uint32_t k) {
+#ifdef __CUDA_ARCH__
+  return k < 8 ? (float)k * 0x1p-9f : __uint_as_float((((k >> 3) + 120u) << 23) | ((k & 7u) << 20));
+#else
+  return (float)e4m3_val(k);
+#endif
+}
 // Bit-level helpers for positive normal doubles (no libm calls on the hot path).
 __device__ __forceinline__ int dexp(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7FF) - 1023; }
 __device__ __forceinline__ double dpow2(int e) { return __longlong_as_double((long long)((uint64_t)(e + 1023) << 52)); }

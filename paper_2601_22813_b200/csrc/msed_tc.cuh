@@ -879,7 +879,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           // two groups side by side, branch-free (independent chains the scheduler can
           // interleave); the rare exact-chunk code fix runs after both
           float gmv[2], mnv[2], s4v[2], dv[2], numv[2], denv[2];
-          double d64v[2];
           bool uncv[2], dokv[2];
           uint32_t c0v[2], c1v[2], mm0[2], mm1[2];
 #pragma unroll
@@ -906,7 +905,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             const float gy = gm * C;                            // ~ gmax
             const float eg = __fmaf_ru(gy, 0x1p-21f, beta);     // |gy - gmax| bound
             float d = 0.f, s4 = 0.f;
-            double d64 = 0.0;
             bool unc = !(gy < 0x1p120f) || (gm == 0.f && beta > 0.f);
             if (MODE == TC_POSTHOC) {
               // pseudo = E8M3_RTN(fl64(gmax / s))  (posthoc.py:82-83)
@@ -925,7 +923,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
                   : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
               const bool live = qs != 0.0 && gm != 0.f;
               unc |= live && (cl != ch || !(isd_hi < 0x1p120f));
-              s4 = live ? (float)e4m3_val(cl) : 0.f;
+              s4 = live ? e4m3_valf(cl) : 0.f;
               // E4M3 (4 significant bits) x scale32 (a float) is exact in double, so its float
               // rounding is one fp32 product; the double value is only needed by the fix path
               d = __fmul_rn(s4, qsf);                           // rounded: inside the code margin
@@ -934,7 +932,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             unc |= sign_chk && !(mnv[gq] > betaY);
             s4v[gq] = s4;
             dv[gq] = d;
-            d64v[gq] = MODE == TC_POSTHOC ? (double)d : (double)s4 * (double)qsf;   // exact
             uncv[gq] = unc;
             dokv[gq] = d > 0.f && !unc;
           }
@@ -986,7 +983,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
                 if (!(((i < 8 ? mm0[gq] : mm1[gq]) >> sh) & 15u)) continue;
                 const double y64 = TAPE ? __dmul_rn(__dmul_rn((double)Y[i], (double)__ldg(a.tape_scale32)), a.inv_sqrt)
                                         : __dmul_rn((double)Y[i], C64);
-                const uint32_t nc = rtn_code_exact(y64, d64v[gq]);
+                const double d64 = MODE == TC_POSTHOC ? (double)dv[gq] : (double)s4v[gq] * (double)qsf;   // exact
+                const uint32_t nc = rtn_code_exact(y64, d64);
                 if (i < 8) c0v[gq] = (c0v[gq] & ~(15u << sh)) | (nc << sh);
                 else c1v[gq] = (c1v[gq] & ~(15u << sh)) | (nc << sh);
               }

@@ -149,10 +149,6 @@ __device__ __noinline__ uint3 quant_group_exact(const void* x, int64_t off, floa
 }
 
 // ---------------------------------------------------------------- fast path --
-// E4M3 value of a code 0..126 as float (exact).
-__device__ __forceinline__ float e4m3_valf(uint32_t k) {
-  return k < 8 ? (float)k * 0x1p-9f : __uint_as_float((((k >> 3) + 120u) << 23) | ((k & 7u) << 20));
-}
 __device__ __forceinline__ uint32_t cvt_e4m3_rn(float y) {
   uint16_t r;
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %1;" : "=h"(r) : "f"(y));
