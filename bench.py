@@ -524,6 +524,22 @@ def extra_configs(q2, args, dev):
             ms = _time_ms(fn, iters=3, warmup=1)
             gbs = n * bpe / (ms / 1e3) / 1e9
             r[tag] = {"ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm}
+        if lg == 24:
+            # the reference's algorithm on the host cores (oracle port), same tensor, one call each
+            x64 = x.double().cpu().numpy()
+            t0 = time.perf_counter()
+            O.quantize_rtn_46(x64)
+            t1 = time.perf_counter()
+            if args.mode == "posthoc":
+                O.posthoc_quantize(x64, O.SeedPair(1, 2), 6.0, 1, 2)
+            else:
+                O.ms_eden_quantize(x64, O.SeedPair(1, 2), 6.0, 1, 2)
+            t2 = time.perf_counter()
+            r["cpu_oracle"] = {"quant_fwd46_ms": (t1 - t0) * 1e3, "msed_rows_ms": (t2 - t1) * 1e3,
+                               "quant_fwd46_GB/s": n * 2.5625 / (t1 - t0) / 1e9,
+                               "msed_rows_GB/s": n * 2.5625 / (t2 - t1) / 1e9, "cores": _threads(),
+                               "kind": "port (oracle/nvfp4_oracle.py, numpy + the reference's loop order)"}
+            del x64
         c2[f"2^{lg}"] = r
         del x
         torch.cuda.empty_cache()
