@@ -829,12 +829,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
       // the split threshold thr), plus flush-to-zero slack.  A chunk without small values is
       // exact.
       float beta = 0.f;
-      if (has_small && nsmall != 0u) {
+      // A chunk with at most one small value has an exact Y2 (one nonzero product per output):
+      // beta = 0, although Y = fl32(Y1 + Y2) still rounds (inside the 2^-21 margins), so only
+      // chunks without small values are exact.
+      if (has_small && nsmall > 1u) {
         const int Eb = TAPE ? (int)(tmaxb >> 10) - 15 - 10 : (int)(tmaxb >> 7) - 127 - 8;   // log2 thr
         const float thr = __uint_as_float((uint32_t)max(Eb + 127, 1) << 23);
         beta = __fmul_ru(__fadd_ru(__fmul_ru(thr * (float)nsmall, 0x1p-19f * 1.0001f), 0x1p-118f), C * 1.0001f);
       }
-      const bool exact_chunk = beta == 0.f && !tiny;          // y64 = fl64(fl64(Y * scale) * c) exactly
+      const bool exact_chunk = (!has_small || nsmall == 0u) && !tiny;   // y64 = fl64(fl64(Y * scale) * c) exactly
       // the sign of a zero / tiny value needs |Y| > betaY -- except an exact zero of an exact
       // chunk without z0, which is +0 in the reference (the fma below makes it +0 here as well)
       const bool sign_chk = !exact_chunk || z0;
@@ -1049,7 +1052,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rdn) : "f"(df));
           const float sq = sqrtf(128.f * nf) * 1.001f;
           const float en = 16.f * 0x1p-24f + (2.f * betaY * sq + 128.f * betaY * betaY) * rn_ * 1.01f;
-          const float ed = 20.f * 0x1p-24f + 2.f * beta * C * sq * rdn * 1.01f;
+          // |d den| <= betaY sum_g d_g sum |sval| <= betaY 2 C sum |Y| <= 2 beta sq (|sval| <= 2 |q|,
+          // q = C Y / d_g, beta = C betaY)
+          const float ed = 20.f * 0x1p-24f + 2.f * beta * sq * rdn * 1.01f;
           // the reference's degenerate test |den| >= 1e-30 num, decided with margin
           ok = df * (1.f - ed) >= 1.001e-30f * (C * nf) * (1.f + en);
           S = C * nf * rdn;
