@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
   const uint32_t bar_mempty = smem_u32(bars + 24);            // [4] tile metadata read (8 warps)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + LY::OFF_MISC);
   // misc: [0] deferred count, [1] tmem base, [2..3] pmax (f32 bits, per orientation), [4..5] running L,
-  //       [8..11] split-warp maxima, [12] flags (bit0 nonfinite, bit1 ovf, bit2 nanscale)
+  //       [8..11] split-warp maxima (tape: scale ranges), [12] flags (bit0 nonfinite, bit1 ovf, bit2
+  //       nanscale), [14..17] split-warp "any small" flags
   uint32_t* deflist = reinterpret_cast<uint32_t*>(smem + LY::OFF_DEF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = a.tiles_r * a.tiles_c;
@@ -688,11 +689,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
           }
       }
       const bool anyw = __any_sync(0xFFFFFFFFu, (anys & 0x7FFF7FFFu) != 0u);
-      if (lane == 0) misc[8 + sw] = anyw ? 1u : 0u;
+      // separate slots from the maxima in misc[8..11]: a warp past pass 2 must not overwrite a
+      // maximum another split warp has not read yet (the absmax pass has no pass 2 in between)
+      if (lane == 0) misc[14 + sw] = anyw ? 1u : 0u;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (st == 0) {
-        const bool hs = (misc[8] | misc[9] | misc[10] | misc[11]) != 0u;
+        const bool hs = (misc[14] | misc[15] | misc[16] | misc[17]) != 0u;
         metau[0] = (hs ? 1u : 0u) | (nonfin ? 2u : 0u) | (tiny ? 4u : 0u);
         metau[9] = M;                                            // tile max |x| bits (bf16 / the tape's f16)
         if (nonfin) misc[12] |= 1u;
