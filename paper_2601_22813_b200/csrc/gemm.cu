@@ -20,6 +20,11 @@
 // MMA needs comes for free), so the MMA thread issues only MMAs.
 //
 // Per CTA (512 threads, one CTA per SM, clusters of 2):
+// Warps 0, 1 and 3 run their loops as whole warps and elect one lane to issue (TMA, MMA,
+// tcgen05.cp): warp-uniform values then live in uniform registers.  A lone-lane issuer
+// wrapped each MMA in an elect/R2UR sequence; with it the tensor pipe was idle ~45% of an
+// MMA-only probe (Q2_GEMM_DBG=4: 4.8 -> 6.4 PFLOP/s once fixed).
+//
 //   warp 0   TMA producer: A/B slices (128 B of K x 128 rows, 128B swizzle)
 //            complete on the LEADER's full barrier (cta_group::2 TMA); the raw
 //            scale halves complete on this CTA's scale barrier.
@@ -75,7 +80,8 @@ struct GemmArgs {
   int M, N, K, kb;                                        // kb = ceil(K/64) scale blocks per row block
   int tiles_m, tiles_n, nk;
   int accumulate;
-  int dbg;                                                // timing probes: 1 = scale warps skip their TMEM writes
+  int dbg;                                                // timing probes (wrong results): 1 = scale warps skip their
+                                                          // TMEM writes, 4 = MMAs re-read the first stages (no feed)
   int sfcp;                                               // 1: the MMA thread copies all scales (tcgen05.cp), no scale warps
   int cpmask;                                             // sfcp == 0: bit s = stage s's scales by the copier thread
   unsigned long long* trace;                              // optional timeline probe (pair 0), else nullptr
@@ -98,6 +104,14 @@ __device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* ma
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & PEER_MASK) : "memory");
+}
+// pair-mode load multicast to the CTAs in `mask` (same shared offset in each); the bytes complete
+// on the barrier at `bar`'s offset in each destination's pair leader
+__device__ __forceinline__ void tma2_load_2d_mc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar,
+                                                uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.cta_group::2 [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & PEER_MASK), "h"(mask) : "memory");
 }
 __device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint32_t bar) {
   asm volatile(
@@ -124,9 +138,14 @@ __device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_
       ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(accum), "r"(tsfa), "r"(tsfb), "r"(IDESC)
       : "memory");
 }
-__device__ __forceinline__ void tc2_commit(uint32_t bar) {   // arrive on `bar` in both CTAs of the pair
+__device__ __forceinline__ bool elect_one() {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(r));
+  return r != 0;
+}
+__device__ __forceinline__ void tc2_commit(uint32_t bar, uint16_t mask) {   // arrive on `bar` in the CTAs of `mask`
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-               ::"r"(bar), "h"((unsigned short)3) : "memory");
+               ::"r"(bar), "h"(mask) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & PEER_MASK) : "memory");
@@ -160,18 +179,42 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tm = first_m + r % gm;
   tn = r / gm;
 }
+// Clusters of CL pairs share one operand: pair p of the cluster takes tile (tm, CL*j + p)
+// (SHARE_A: the A rows are common) or (CL*i + p, tn) (B common).  A cluster walks "super
+// tiles"; a pair whose tile falls past the matrix edge still loads and multiplies (zeros)
+// because the others need its slice of the shared operand, and stores nothing.
+template <int CL, bool SHARE_A>
+__device__ __forceinline__ int super_count(const GemmArgs& g) {
+  return SHARE_A ? g.tiles_m * ((g.tiles_n + CL - 1) / CL) : ((g.tiles_m + CL - 1) / CL) * g.tiles_n;
+}
+template <int CL, bool SHARE_A>
+__device__ __forceinline__ void super_coords(int u, const GemmArgs& g, int p, int& tm, int& tn) {
+  if (SHARE_A) {
+    tile_coords(u, g.tiles_m, (g.tiles_n + CL - 1) / CL, tm, tn);
+    tn = tn * CL + p;
+  } else {
+    tile_coords(u, (g.tiles_m + CL - 1) / CL, g.tiles_n, tm, tn);
+    tm = tm * CL + p;
+  }
+}
 
-template <bool F32>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+template <bool F32, int CL, bool SHARE_A>
+__global__ void __cluster_dims__(2 * CL, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     nvfp4_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                       GemmArgs g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays a shared-space pointer (LDS/STS, not generic LD/ST)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int ntiles = g.tiles_m * g.tiles_n;
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1, pp = crank >> 1;           // CTA within the pair, pair within the cluster
+  const int clid = blockIdx.x / (2 * CL), ncl = gridDim.x / (2 * CL);
+  const int nsuper = super_count<CL, SHARE_A>(g);
+  const bool tr0 = clid == 0 && pp == 0;                      // the traced pair
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pp));
+  const uint16_t all_mask = (uint16_t)((1u << (2 * CL)) - 1);
+  constexpr uint32_t SL = 128 / CL;                           // rows of the shared operand each pair loads
+  constexpr uint16_t MC = CL == 4 ? 0x55 : (CL == 2 ? 0x5 : 0x1);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   const uint32_t bar_full = smem_u32(bars);                   // A/B of both CTAs (leader's copy used)
@@ -186,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_sff + 8 * s, 1);
       mbar_init(bar_sfr + 8 * s, (g.cpmask >> s) & 1 ? 1 : 8);  // copier commit / 4 scale warps x 2 CTAs
-      mbar_init(bar_empty + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, CL);                        // one MMA commit per pair of the cluster
     }
     mbar_init(bar_accf, 1);
     mbar_init(bar_acce, 16);                                  // 8 epilogue warps x 2 CTAs
@@ -210,57 +253,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ---------------- TMA producer (both CTAs) ----------------
+      // whole warp in the loop, one elected lane issues (as the MMA issuer)
       int it = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
+      const uint16_t mc = (uint16_t)(MC << rank);             // this CTA's counterparts in every pair
+      for (int u = clid; u < nsuper; u += ncl) {
         int tm, tn;
-        tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
+        super_coords<CL, SHARE_A>(u, g, (int)pp, tm, tn);
         const int m0 = tm * PT + (int)rank * 128, n0 = tn * PT + (int)rank * 128;
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
+          if (g.dbg >= 4 && it >= STAGES) break;              // probe: MMAs re-read the first stages
+          // the stage is free in every CTA this one writes: each pair's MMA commit arrives here
           if (it >= STAGES) mbar_wait_sleep(bar_empty + 8 * s, ((it / STAGES) - 1) & 1);
+          if (!elect_one()) { __syncwarp(); continue; }
           const uint32_t st = smem_u32(smem + s * STAGE), fb = bar_full + 8 * s, sb = bar_sff + 8 * s;
-          if (g.sfcp || ((g.cpmask >> s) & 1)) {
-            // scales of both CTAs complete on the leader's full barrier with the operands
-            if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST + SFA_ST + SFB_ST));
+          const bool cps = g.sfcp || ((g.cpmask >> s) & 1);
+          // scales of copier stages complete on the leader's full barrier with the operands
+          if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST + (cps ? SFA_ST + SFB_ST : 0)));
+          if (CL == 1) {
             tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
             tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
+          } else if (SHARE_A) {                                 // slice pp of the common A rows, to all pairs
+            tma2_load_2d_mc(st + pp * SL * BKB, &tmA, kt * BKB, m0 + (int)(pp * SL), fb, mc);
+            tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
+          } else {
+            tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
+            tma2_load_2d_mc(st + A_ST + pp * SL * BKB, &tmB, kt * BKB, n0 + (int)(pp * SL), fb, mc);
+          }
+          if (cps) {
             tma2_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, fb);
             tma2_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, fb);
-            continue;
+          } else {
+            mbar_expect_tx(sb, SFA_ST + SFB_ST);
+            tma_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, sb);
+            tma_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, sb);
           }
-          if (rank == 0) mbar_expect_tx(fb, 2 * (A_ST + B_ST));
-          tma2_load_2d(st, &tmA, kt * BKB, m0, fb);
-          tma2_load_2d(st + A_ST, &tmB, kt * BKB, n0, fb);
-          mbar_expect_tx(sb, SFA_ST + SFB_ST);
-          tma_load_3d(st + A_ST + B_ST, &tmSFA, 0, (int)rank, (tm * g.kb + 4 * kt) * 4, sb);
-          tma_load_3d(st + A_ST + B_ST + SFA_ST, &tmSFB, 0, 0, (tn * g.kb + 4 * kt) * 4, sb);
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
       // ---------------- MMA issuer (leader) ----------------
+      // The whole warp runs the loop (warp-uniform values stay in uniform registers) and one
+      // elected lane issues each stage's MMAs: a lone-lane loop wrapped every MMA in an
+      // elect/R2UR sequence and left the tensor pipe idle ~45% of the time (ncu, MMA-only probe).
       int it = 0, tc = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++tc) {
+      for (int u = clid; u < nsuper; u += ncl, ++tc) {
         if (tc >= 1) mbar_wait(bar_acce, (tc - 1) & 1);       // both epilogues drained the accumulator
         tc_fence_after();
-        if (g.trace && pair == 0 && tc < 64) g.trace[4 * tc] = gtime();
+        if (g.trace && tr0 && tc < 64 && lane == 0) g.trace[4 * tc] = gtime();
         unsigned long long wf = 0, ws = 0;
         for (int kt = 0; kt < g.nk; ++kt, ++it) {
           const int s = it % STAGES;
           const unsigned long long t0 = g.trace ? gtime() : 0;
-          mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
+          if (g.dbg < 4 || it < STAGES) mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
           const unsigned long long t1 = g.trace ? gtime() : 0;
-          if (!g.sfcp) mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
+          if (!g.sfcp && (g.dbg < 4 || it < STAGES)) mbar_wait(bar_sfr + 8 * s, (it / STAGES) & 1);
           if (g.trace) { wf += t1 - t0; ws += gtime() - t1; }
           tc_fence_after();
           const uint32_t st = smem_u32(smem + s * STAGE);
           const uint64_t adesc = desc_sw128(st), bdesc = desc_sw128(st + A_ST);
           const uint32_t tsf = tmem + SF_COL + SF_SLOT * s;
           const int nsub = min(4, g.K / 64 - 4 * kt);          // K tail: no MMA past K
-          if (g.sfcp) {
+          const bool leader = elect_one();
+          if (g.sfcp && leader) {
             // scales of this stage into its own TMEM slot (distinct per stage and K64 block, so
             // the copies never wait on an MMA still reading the previous contents); the tensor
             // pipe runs them in issue order ahead of the MMAs that read them.  32x128b.warpx4
@@ -274,15 +333,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
               tc2_cp_sf(tsf + 12 * kk + 8, desc_sf32(sfb + 1024 * kk + 128, 256));
             }
           }
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            if (kk >= nsub) break;
-            tc2_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, tsf + 12 * kk, tsf + 12 * kk + 4, (kt | kk) != 0);
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk >= nsub) break;
+              tc2_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, tsf + 12 * kk, tsf + 12 * kk + 4, (kt | kk) != 0);
+            }
+            tc2_commit(bar_empty + 8 * s, all_mask);
           }
-          tc2_commit(bar_empty + 8 * s);
+          __syncwarp();
         }
-        tc2_commit(bar_accf);
-        if (g.trace && pair == 0 && tc < 64) { g.trace[4 * tc + 1] = gtime(); g.trace[256 + 2 * tc] = wf; g.trace[257 + 2 * tc] = ws; }
+        if (elect_one()) tc2_commit(bar_accf, pair_mask);
+        __syncwarp();
+        if (g.trace && tr0 && tc < 64 && lane == 0) { g.trace[4 * tc + 1] = gtime(); g.trace[256 + 2 * tc] = wf; g.trace[257 + 2 * tc] = ws; }
       }
     }
   } else if (warp == 3 && g.cpmask) {
@@ -292,14 +355,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // beyond the 6 KB of the stage, so splitting stages between this thread and the scale
     // warps balances the pipe against shared-memory bandwidth; with few K stages per tile
     // the copier runs ahead while the MMA waits for the accumulator drain.
-    if (rank == 0 && lane == 0) {
-      const int my_tiles = pair < ntiles ? (ntiles - 1 - pair) / npairs + 1 : 0;
+    if (rank == 0) {
+      const int my_tiles = clid < nsuper ? (nsuper - 1 - clid) / ncl + 1 : 0;
       const int total = my_tiles * g.nk;
       for (int it = 0; it < total; ++it) {
         const int s = it % STAGES, kt = it % g.nk;
         if (!((g.cpmask >> s) & 1)) continue;
         mbar_wait(bar_full + 8 * s, (it / STAGES) & 1);
         tc_fence_after();
+        if (!elect_one()) { __syncwarp(); continue; }
         const uint32_t st = smem_u32(smem + s * STAGE), sfa = st + A_ST + B_ST, sfb = sfa + SFA_ST;
         const uint32_t tsf = tmem + SF_COL + SF_SLOT * s;
         const int nsub = min(4, g.K / 64 - 4 * kt);
@@ -311,7 +375,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tc2_cp_sf(tsf + 12 * kk + 8, desc_sf32(sfb + 1024 * kk + 128, 256));
         }
         asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                     ::"r"(bar_sfr + 8 * s), "h"((unsigned short)1) : "memory");
+                     ::"r"(bar_sfr + 8 * s), "h"((unsigned short)(1u << (2 * pp))) : "memory");
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 8 && !g.sfcp && g.cpmask != (1 << STAGES) - 1) {
@@ -323,10 +388,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // Stages are written two at a time with one tcgen05.wait::st: the per-stage chain
     // (LDS -> STTM -> wait -> fence -> remote arrive) is longer than a stage's MMAs, so
     // one stage per round left the MMA waiting on scales.
-    const int my_tiles = pair < ntiles ? (ntiles - 1 - pair) / npairs + 1 : 0;
+    const int my_tiles = clid < nsuper ? (nsuper - 1 - clid) / ncl + 1 : 0;
     const int total = my_tiles * g.nk;
-    for (int it = 0; it < total; it += Q2_SF_BATCH) {
-      const int nb = min(Q2_SF_BATCH, total - it);
+    for (int it = 0; it < (g.dbg >= 4 ? min(total, STAGES) : total); it += Q2_SF_BATCH) {
+      const int nb = min(Q2_SF_BATCH, (g.dbg >= 4 ? min(total, STAGES) : total) - it);
 #pragma unroll
       for (int u = 0; u < Q2_SF_BATCH; ++u) {
         if (u >= nb) break;
@@ -363,12 +428,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const float alpha = __ldg(g.sa) * __ldg(g.sb);
     const uint32_t tbase = tmem + ((uint32_t)(sp * 32) << 16) + grp * 128;
     int tc = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++tc) {
+    for (int u = clid; u < nsuper; u += ncl, ++tc) {
       int tm, tn;
-      tile_coords(t, g.tiles_m, g.tiles_n, tm, tn);
+      super_coords<CL, SHARE_A>(u, g, (int)pp, tm, tn);
       mbar_wait_sleep(bar_accf, tc & 1);
       tc_fence_after();
-      if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 2] = gtime();
+      if (g.trace && tr0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 2] = gtime();
       const int gm = tm * PT + (int)rank * 128 + row, gn0 = tn * PT + grp * 128;
       unsigned char* drow = static_cast<unsigned char*>(g.d) + (int64_t)gm * g.ldd * (F32 ? 4 : 2);
       if (!F32) {
@@ -388,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_leader(bar_acce);          // MMA may overwrite the accumulator
-        if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
+        if (g.trace && tr0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
         __nv_bfloat16* dr = reinterpret_cast<__nv_bfloat16*>(drow);
         if (Q2_GEMM_STAGE_EPI && tm * PT + (int)rank * 128 + 128 <= g.M && gn0 + 128 <= g.N) {
           // coalesced stores: the warp's 32 rows x 64 columns go through 4 KB of shared memory
@@ -459,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(bar_acce);        // MMA may overwrite the accumulator
-          if (g.trace && pair == 0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
+          if (g.trace && tr0 && rank == 0 && warp == 8 && lane == 0 && tc < 64) g.trace[4 * tc + 3] = gtime();
         }
         if (F32 && Q2_GEMM_STAGE_EPI && tm * PT + (int)rank * 128 + 128 <= g.M && gn0 + 128 <= g.N) {
           // coalesced fp32 stores (and accumulate reads) through the warp's 4 KB of shared memory
@@ -544,19 +609,57 @@ static bool make_sf_map(CUtensorMap* map, const void* sf, int64_t R, int64_t K, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool F32>
+// Persistent grid: as many clusters as fit at once (clusters of 8 CTAs may not tile every
+// GPC, so the count comes from the occupancy query, once per device).
+template <bool F32, int CL, bool SHARE_A>
 static int launch_gemm(const CUtensorMap* maps, const GemmArgs& g, cudaStream_t st) {
+  auto kern = nvfp4_gemm_kernel<F32, CL, SHARE_A>;
   static unsigned attr = 0;                     // per-device opt-in
-  if (!smem_opt_in(nvfp4_gemm_kernel<F32>, GEMM_SMEM, attr)) return Q2_ECUDA;
+  static int max_cl[64] = {0};
+  if (!smem_opt_in(kern, GEMM_SMEM, attr)) return Q2_ECUDA;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int ntiles = g.tiles_m * g.tiles_n;
-  const int npairs = std::max(1, std::min(ntiles, nsm / 2));
-  if (launch_pdl(nvfp4_gemm_kernel<F32>, dim3(2 * npairs), dim3(GEMM_THREADS), GEMM_SMEM, st, maps[0], maps[1],
+  int& mc = max_cl[dev & 63];
+  if (mc == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nsm / (2 * CL) * 2 * CL);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = GEMM_SMEM;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = nsm / (2 * CL);
+    }
+    mc = n;
+    if (getenv("Q2_GEMM_VERBOSE")) fprintf(stderr, "gemm: clusters of %d pairs, %d resident\n", CL, n);
+  }
+  const int nsuper = SHARE_A ? g.tiles_m * ((g.tiles_n + CL - 1) / CL) : ((g.tiles_m + CL - 1) / CL) * g.tiles_n;
+  const int ncl = std::max(1, std::min(nsuper, mc));
+  if (launch_pdl(kern, dim3(2 * CL * ncl), dim3(GEMM_THREADS), GEMM_SMEM, st, maps[0], maps[1],
                  maps[2], maps[3], g) != cudaSuccess)
     return Q2_ECUDA;
   return Q2_OK;
+}
+
+// Pairs per cluster and the shared operand: clusters of CL pairs read the common operand
+// from L2 once (TMA multicast) -- the kernel is L2-throughput bound otherwise (ncu: LTS at
+// ~52% of its nominal peak = the chip's practical cap).  Prefer the side that divides evenly.
+template <bool F32>
+static int dispatch_gemm(const q2_nvfp4* a, const q2_nvfp4* b, const CUtensorMap* maps, GemmArgs& g,
+                         cudaStream_t st, int cl) {
+  const bool share_a = g.tiles_n % cl == 0 || g.tiles_m % cl != 0;
+  if (cl > 1) {
+    // the shared operand's map loads 128/cl-row slices
+    const int sl = 128 / cl;
+    CUtensorMap* m = const_cast<CUtensorMap*>(maps);
+    const bool ok = share_a ? make_map(&m[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, a->codes, a->K / 2, a->R, a->K / 2, BKB, sl)
+                            : make_map(&m[1], CU_TENSOR_MAP_DATA_TYPE_UINT8, b->codes, b->K / 2, b->R, b->K / 2, BKB, sl);
+    if (!ok) return Q2_ECUDA;
+  }
+  if (cl == 4) return share_a ? launch_gemm<F32, 4, true>(maps, g, st) : launch_gemm<F32, 4, false>(maps, g, st);
+  if (cl == 2) return share_a ? launch_gemm<F32, 2, true>(maps, g, st) : launch_gemm<F32, 2, false>(maps, g, st);
+  return launch_gemm<F32, 1, true>(maps, g, st);
 }
 
 }  // namespace q2
@@ -593,7 +696,12 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
              getenv("Q2_GEMM_TRACE") ? trace : nullptr};
   if (g.trace) cudaMemsetAsync(trace, 0, 64 * 8 * 8, static_cast<cudaStream_t>(stream));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int rc = d_dtype == Q2_F32 ? launch_gemm<true>(maps, g, st) : launch_gemm<false>(maps, g, st);
+  // clusters of 2 or 4 pairs multicasting the shared operand: measured slower (the occupancy
+  // query gives 33 / 15 resident clusters = 132 / 120 SMs, and the per-SM rate does not rise:
+  // multicast to <= 4 CTAs costs L2 like unicast), kept as an A/B option
+  static const int g_cl = getenv("Q2_GEMM_CL") ? atoi(getenv("Q2_GEMM_CL")) : 1;
+  const int cl = g_cl == 4 ? 4 : (g_cl == 2 ? 2 : 1);
+  const int rc = d_dtype == Q2_F32 ? dispatch_gemm<true>(a, b, maps, g, st, cl) : dispatch_gemm<false>(a, b, maps, g, st, cl);
   if (g.trace) {
     unsigned long long h[512];
     cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);

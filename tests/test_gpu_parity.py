@@ -141,7 +141,7 @@ def _gemm_check(d, qa_ref, qb_ref, bf16):
 
 
 @pytest.mark.parametrize("mnk", [(128, 256, 256), (256, 512, 1024), (384, 640, 320), (200, 136, 192),
-                                 (1024, 768, 2048)])
+                                 (1024, 768, 2048), (1280, 768, 512), (768, 1280, 512), (2048, 1792, 256)])
 @pytest.mark.parametrize("bf16_out", [False, True])
 def test_gemm(cuda, mnk, bf16_out):
     q2 = _q2()
