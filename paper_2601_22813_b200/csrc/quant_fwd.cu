@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(QT + 32, Q2_QMINB) quant_fwd_kernel(
 // groups it still cannot certify the literal float64 restatement
 // (quant_group_exact).  No shared-memory ring, no block barriers, no fix-up lists.
 #ifndef Q2_QDMINB
-#define Q2_QDMINB 4
+#define Q2_QDMINB 3
 #endif
 constexpr int QD_THREADS = 256;
 constexpr int QD_CAP = 256;                               // per-warp queue of undecided groups
@@ -632,10 +632,19 @@ __global__ void __launch_bounds__(QD_THREADS, Q2_QDMINB) quant_fwd_direct_kernel
   // loop bounds on the warp's first group (gid - lane): every lane runs the same iterations
   // (the ballots below need the full warp); lanes past either end are simply not live
   for (;;) {
+  // the next group's 32 (64) bytes are requested before this group's arithmetic: the
+  // first use of a load was the top stall (long scoreboard, ~20% of samples)
+  uint32_t wn[16];
+  load_group<DT>(x, gid, gid >= 0 && gid < total, wn);
   for (; gid - lane > -nth - 31; gid -= nth) {
     const bool live = gid >= 0 && gid < total;
     uint32_t w[16];
-    load_group<DT>(x, gid, live, w);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = wn[i];
+    {
+      const int64_t g2 = gid - nth;
+      load_group<DT>(x, g2, g2 >= 0 && g2 < total, wn);
+    }
     uint32_t lo = 0, hi = 0, s8 = 0;
     bool fix = false;
     if (live && amax != 0.f) {
