@@ -138,11 +138,6 @@ __device__ __forceinline__ void tc2_mma(uint32_t tmem_d, uint64_t adesc, uint64_
       ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(accum), "r"(tsfa), "r"(tsfb), "r"(IDESC)
       : "memory");
 }
-__device__ __forceinline__ bool elect_one() {
-  uint32_t r;
-  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(r));
-  return r != 0;
-}
 __device__ __forceinline__ void tc2_commit(uint32_t bar, uint16_t mask) {   // arrive on `bar` in the CTAs of `mask`
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                ::"r"(bar), "h"(mask) : "memory");

@@ -445,7 +445,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ----------------------------------------------------------------- MMA
-    if (lane == 0) {
+    // whole warp in the loop, one elected lane issues (warp-uniform descriptors stay in
+    // uniform registers; a lone-lane loop paid an elect/R2UR sequence per MMA)
+    {
       // M = 128 (chunks), N = 64 (one output half), bf16 x bf16 -> f32
       const uint32_t ab_fmt = TAPE ? 0u : 1u;                 // f16 (tape) / bf16 operands
       const uint32_t idk = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
@@ -471,23 +473,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
             tc_fence_after();
             const uint32_t id = idk | (o ? (1u << 15) : 0u);
             const uint32_t bb = smem_u32(smem + LY::OFF_B + jj * 32768) + 8192 * h;   // B rows 64h..64h+63
+            if (elect_one()) {
 #pragma unroll
-            for (int part = 0; part < 2; ++part) {
-              if (part == 1 && (!has_small || a.dbg == 3)) break;
-              if (a.dbg == 4) break;
-              const uint32_t ab = part ? smallb : mainb;
+              for (int part = 0; part < 2; ++part) {
+                if (part == 1 && (!has_small || a.dbg == 3)) break;
+                if (a.dbg == 4) break;
+                const uint32_t ab = part ? smallb : mainb;
 #pragma unroll
-              for (int kk = 0; kk < 8; ++kk) {
-                const uint64_t ad = o == 0 ? desc_sw128(ab + (kk >> 2) * 16384 + (kk & 3) * 32)
-                                           : desc_mn_sw128(ab + kk * 2048, 16384, 1024);
-                const uint64_t bd = desc_sw128(bb + (kk >> 2) * 16384 + (kk & 3) * 32);
-                tc_mma_f16(tmem + 256 * buf + 128 * h + 64 * part, ad, bd, id, kk > 0);
+                for (int kk = 0; kk < 8; ++kk) {
+                  const uint64_t ad = o == 0 ? desc_sw128(ab + (kk >> 2) * 16384 + (kk & 3) * 32)
+                                             : desc_mn_sw128(ab + kk * 2048, 16384, 1024);
+                  const uint64_t bd = desc_sw128(bb + (kk >> 2) * 16384 + (kk & 3) * 32);
+                  tc_mma_f16(tmem + 256 * buf + 128 * h + 64 * part, ad, bd, id, kk > 0);
+                }
               }
+              tc_commit(bar_tfull + 8 * (2 * buf + h));
             }
-            tc_commit(bar_tfull + 8 * (2 * buf + h));
+            __syncwarp();
           }
         }
-        tc_commit(bar_sempty + 8 * s);
+        if (elect_one()) tc_commit(bar_sempty + 8 * s);
+        __syncwarp();
       }
     }
   } else if (warp < 6) {
