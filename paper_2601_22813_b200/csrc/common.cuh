@@ -58,7 +58,9 @@ __host__ __device__ __forceinline__ double e4m3_val(uint32_t code) {
 // The same value as a float (exact): code < 8 is k * 2^-9, else (8 + m) 2^(e-10).
 __host__ __device__ __forceinline__ float e4m3_valf(uint32_t k) {
 #ifdef __CUDA_ARCH__
-  return k < 8 ? (float)k * 0x1p-9f : __uint_as_float((((k >> 3) + 120u) << 23) | ((k & 7u) << 20));
+  // k * 2^-9 as one exact FMA on (2^23 + k) (no int->float conversion on the XU pipe)
+  return k < 8 ? __fmaf_rn(__uint_as_float(0x4B000000u | k), 0x1p-9f, -0x1p14f)
+               : __uint_as_float((((k >> 3) + 120u) << 23) | ((k & 7u) << 20));
 #else
   return (float)e4m3_val(k);
 #endif

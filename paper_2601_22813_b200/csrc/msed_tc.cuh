@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
               asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %3;\n\tcvt.u32.u16 %0, t;\n\t}\n\t"
                   "{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %2, %4;\n\tcvt.u32.u16 %1, t;\n\t}"
                   : "=r"(cl), "=r"(ch) : "f"(0.f), "f"(fmaxf(lo, 0.f)), "f"(hi));
-              const bool live = qs != 0.0 && gm != 0.f;
+              const bool live = qsf != 0.f && gm != 0.f;          // float test: a double one ran per group on the FP64 pipe
               unc |= live && (cl != ch || !(isd_hi < 0x1p120f));
               s4 = live ? e4m3_valf(cl) : 0.f;
               // E4M3 (4 significant bits) x scale32 (a float) is exact in double, so its float
@@ -1095,13 +1095,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) msed_tc_kernel(const __grid_con
               *reinterpret_cast<uint4*>(oaw + g0) = make_uint4(aws[0] | (aws[1] << 16), aws[2] | (aws[3] << 16),
                                                                aws[4] | (aws[5] << 16), aws[6] | (aws[7] << 16));
             } else {
+              // E4M3 codes: the normal range (E in [-6, 8): eb in [250, 264)) by one shift-add of
+              // each word, branch-free; a chunk with any other live word redoes all eight through
+              // aword_code (subnormal RTN, overflow)
               uint32_t w0 = 0, w1 = 0;
+              bool slow = false;
 #pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                bool o2 = false, o3 = false;
-                w0 |= aword_code_fast(aws[g], 0, &o2) << (8 * g);
-                w1 |= aword_code_fast(aws[g + 4], 0, &o3) << (8 * g);
-                if (o2 || o3) ovf = true;
+              for (int g = 0; g < 8; ++g) {
+                const uint32_t w = aws[g], eb = w >> 7;
+                slow |= w != 0u && (eb < 250u || eb >= 264u);
+                const uint32_t c = w == 0u ? 0u : (w >> 4) + ((w >> 3) & 1u) - (249u << 3);
+                if (g < 4) w0 |= (c & 0xFFu) << (8 * g);
+                else w1 |= (c & 0xFFu) << (8 * (g - 4));
+              }
+              if (slow) {
+                w0 = 0u; w1 = 0u;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                  bool o2 = false, o3 = false;
+                  w0 |= aword_code_fast(aws[g], 0, &o2) << (8 * g);
+                  w1 |= aword_code_fast(aws[g + 4], 0, &o3) << (8 * g);
+                  if (o2 || o3) ovf = true;
+                }
               }
               *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8, okb)) = w0;
               *reinterpret_cast<uint32_t*>(osf + sf_offset(r, ci * 8 + 4, okb)) = w1;
