@@ -215,6 +215,9 @@ def main():
     ap.add_argument("--mode", default="posthoc", choices=["posthoc", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the c1 / c2 / c5 configs")
+    ap.add_argument("--dw-reduce", default="auto", choices=["auto", "nccl", "multimem"],
+                    help="N > 1: dW sum by NCCL all-reduce or inside the wgrad GEMM over NVLS multicast "
+                         "(auto: multimem when the group has a multicast object)")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of the captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -239,6 +242,13 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     q2.set_error_mode("deferred")
 
+    from paper_2601_22813_b200.parallel import MulticastReducer
+    dw_reduce = args.dw_reduce
+    if world == 1:
+        dw_reduce = "none"
+    elif dw_reduce == "auto":
+        dw_reduce = "multimem" if MulticastReducer.available() else "nccl"
+
     g = torch.Generator(device=dev)
     data = []
     for pi, (name, din, dout) in enumerate(PROJECTIONS):
@@ -251,7 +261,8 @@ def main():
 
     def measure(mode):
         """Captured-graph (N=1) or eager (N>1) step time of one MS-EDEN mode, max over ranks."""
-        runner = ShardedLinearStep(q2.LayerConfig(posthoc=mode == "posthoc"), rank=rank, world=world)
+        runner = ShardedLinearStep(q2.LayerConfig(posthoc=mode == "posthoc"), rank=rank, world=world,
+                                   reduce="multimem" if dw_reduce == "multimem" else "nccl")
         for i in range(args.warmup):
             runner.step(data, i)
         torch.cuda.synchronize()
@@ -317,6 +328,7 @@ def main():
         "config": {"workload": "c3: Llama-1.9B-class projections qkv/o/upgate/down (d=2048, ffn=5632), "
                                f"{TOKENS} tokens per GPU, fwd+bwd", "tokens_per_gpu": TOKENS,
                    "msed_mode": args.mode, "parallelism": f"token-sharded dp{world}" if world > 1 else "single",
+                   "dw_reduce": dw_reduce,
                    "l2": "inputs larger than L2 (>1 GB streamed per step), no flush", "launch": launch},
         "speedup_vs_bf16": bf16_ms / ms, "bf16_cublas_ms_per_step": bf16_ms, "modes": modes,
         "kernels": detail["kernels"], "roofline": detail["roofline"], "rooflines": detail["rooflines"],

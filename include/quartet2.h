@@ -224,6 +224,17 @@ int q2_quant_square_block(const void* x, int dtype, int64_t R, int64_t C, int us
  * K % 64 == 0; K/2 % 16 == 0.                                                */
 int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_dtype, int64_t ldd,
                int accumulate, void* stream);
+/* accumulate (fp32 output only beyond Q2_ACC_STORE):
+ *   Q2_ACC_STORE    D = A.B^T
+ *   Q2_ACC_ADD      D += A.B^T (read-add-store; this launch is D's only writer)
+ *   Q2_ACC_RED      D += A.B^T by red.global.add.v4.f32 (concurrent writers allowed)
+ *   Q2_ACC_MULTIMEM d is an NVLS multicast address (cuMulticast / torch symmetric memory):
+ *                   multimem.red.add.v4.f32 adds the tile into every member GPU's copy of D,
+ *                   i.e. the data-parallel dW all-reduce fused into the wgrad epilogue
+ *                   (replaces the dist.all_reduce after linear_graph.py:322-326).  The caller
+ *                   zeroes D on every rank and barriers before, and barriers after, the launches.
+ * Reductions flush fp32 subnormals (REDG .FTZ).                                              */
+enum { Q2_ACC_STORE = 0, Q2_ACC_ADD = 1, Q2_ACC_RED = 2, Q2_ACC_MULTIMEM = 3 };
 
 /* Helpers used by the host mirror: dequantize (quantizers.py:315-323) into
  * float64 [R, K]; unpack codes/scales into the reference's unpacked layout

@@ -17,6 +17,7 @@ Q2_OK, Q2_EINVAL, Q2_ECUDA = 0, 1, 2
 Q2_BF16, Q2_F32, Q2_F64 = 0, 1, 2
 Q2_SRC_ROWS, Q2_SRC_COLS, Q2_SRC_TAPE_COLS = 0, 1, 2
 Q2_MSED_EXACT, Q2_MSED_POW2, Q2_MSED_POSTHOC = 0, 1, 2
+Q2_ACC_STORE, Q2_ACC_ADD, Q2_ACC_RED, Q2_ACC_MULTIMEM = 0, 1, 2, 3
 Q2_ERR_NONFINITE, Q2_ERR_SCALE448, Q2_ERR_NAN_SCALE, Q2_ERR_E8M3_OVF, Q2_ERR_SR_CLIP = 1, 2, 4, 8, 16
 
 # Every symbol include/quartet2.h declares (checked by tests/test_abi.py).

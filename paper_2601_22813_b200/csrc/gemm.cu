@@ -92,6 +92,28 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// fp32 epilogue writes by accumulate mode: 0 store, 1 read-add-store (one writer per element),
+// Q2_ACC_RED: red.global.add (any number of concurrent writers, e.g. split work on this GPU),
+// Q2_ACC_MULTIMEM: d is an NVLS multicast address; the switch adds the tile into every member
+// GPU's replica (the fused wgrad all-reduce).  The reductions flush subnormals.
+__device__ __forceinline__ void out_f32x4(float* dp, float4 o, int mode) {
+  if (mode == 3) {
+    asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(dp), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w) : "memory");
+  } else if (mode == 2) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                 :: "l"(dp), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w) : "memory");
+  } else {
+    if (mode == 1) { const float4 p = *reinterpret_cast<const float4*>(dp); o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w; }
+    *reinterpret_cast<float4*>(dp) = o;
+  }
+}
+__device__ __forceinline__ void out_f32(float* dp, float o, int mode) {
+  if (mode == 3) asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" :: "l"(dp), "f"(o) : "memory");
+  else if (mode == 2) asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" :: "l"(dp), "f"(o) : "memory");
+  else *dp = mode == 1 ? *dp + o : o;
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -539,8 +561,7 @@ __global__ void __cluster_dims__(2 * CL, 1, 1) __launch_bounds__(GEMM_THREADS, 1
               const int r = 4 * i + lr;
               float4 o = *reinterpret_cast<const float4*>(stg + r * 128 + ((lc ^ (r & 7)) << 4));
               float* dp = static_cast<float*>(g.d) + (row0 + r) * g.ldd + gn0 + 64 * half + 32 * q + 4 * lc;
-              if (g.accumulate) { const float4 pv = *reinterpret_cast<const float4*>(dp); o.x += pv.x; o.y += pv.y; o.z += pv.z; o.w += pv.w; }
-              *reinterpret_cast<float4*>(dp) = o;
+              out_f32x4(dp, o, g.accumulate);
             }
             __syncwarp();
           }
@@ -557,11 +578,10 @@ __global__ void __cluster_dims__(2 * CL, 1, 1) __launch_bounds__(GEMM_THREADS, 1
                                      alpha * __uint_as_float(v[q][c8 + 2]), alpha * __uint_as_float(v[q][c8 + 3]));
               float* dp = reinterpret_cast<float*>(drow) + n;
               if (n + 4 <= g.N) {
-                if (g.accumulate) { const float4 p = *reinterpret_cast<const float4*>(dp); o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w; }
-                *reinterpret_cast<float4*>(dp) = o;
+                out_f32x4(dp, o, g.accumulate);
               } else {
                 const float oo[4] = {o.x, o.y, o.z, o.w};
-                for (int i = 0; i < 4 && n + i < g.N; ++i) dp[i] = g.accumulate ? dp[i] + oo[i] : oo[i];
+                for (int i = 0; i < 4 && n + i < g.N; ++i) out_f32(dp + i, oo[i], g.accumulate);
               }
             } else {
               uint32_t p[4];
@@ -583,6 +603,9 @@ __global__ void __cluster_dims__(2 * CL, 1, 1) __launch_bounds__(GEMM_THREADS, 1
       }
     }
   }
+  // multicast reductions performed system-wide before the kernel retires, so the caller's
+  // cross-GPU barrier after this launch orders them (release side of that barrier)
+  if (F32 && g.accumulate == 3) asm volatile("fence.acq_rel.sys;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   cluster_sync();                                             // peer's MMAs/arrivals done before teardown
@@ -665,7 +688,7 @@ extern "C" int q2_gemm_tn(const q2_nvfp4* a, const q2_nvfp4* b, void* d, int d_d
                           void* stream) {
   if (!a || !b || !d || a->K != b->K || a->K % 64 || (a->K / 2) % 16 || a->R <= 0 || b->R <= 0) return Q2_EINVAL;
   if (d_dtype != Q2_BF16 && d_dtype != Q2_F32) return Q2_EINVAL;
-  if (accumulate && d_dtype != Q2_F32) return Q2_EINVAL;
+  if (accumulate < Q2_ACC_STORE || accumulate > Q2_ACC_MULTIMEM || (accumulate && d_dtype != Q2_F32)) return Q2_EINVAL;
   const int esz = d_dtype == Q2_F32 ? 4 : 2;
   if (ldd < b->R || (ldd * esz) % 16 || (reinterpret_cast<uintptr_t>(d) & 15)) return Q2_EINVAL;
   if (a->R > INT32_MAX || b->R > INT32_MAX || a->K > INT32_MAX) return Q2_EINVAL;

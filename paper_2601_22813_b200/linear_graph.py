@@ -154,9 +154,26 @@ class GradPair:
     dW: torch.Tensor
 
 
+_ACC_MODES = {False: _lib.Q2_ACC_STORE, True: _lib.Q2_ACC_ADD, "store": _lib.Q2_ACC_STORE,
+              "add": _lib.Q2_ACC_ADD, "red": _lib.Q2_ACC_RED, "multimem": _lib.Q2_ACC_MULTIMEM}
+
+
 def gemm(qa: NVFP4Tensor, qb: NVFP4Tensor, out_dtype=torch.float32, out: torch.Tensor = None,
-         accumulate: bool = False) -> torch.Tensor:
-    """D = dequant(qa) . dequant(qb)^T on the tcgen05 NVFP4 kernel (FP32 accumulation)."""
+         accumulate=False, multicast_ptr: int = 0) -> torch.Tensor:
+    """D = dequant(qa) . dequant(qb)^T on the tcgen05 NVFP4 kernel (FP32 accumulation).
+
+    ``accumulate``: False / "store" (D = A.B^T), True / "add" (D += A.B^T, this call is the
+    only writer), "red" (D += A.B^T by atomic reductions: concurrent writers allowed) or
+    "multimem" (the epilogue adds the tile into every rank's replica of ``out`` through the
+    NVLS multicast address ``multicast_ptr`` of ``out``'s symmetric buffer: the dW
+    all-reduce fused into the wgrad GEMM; see ``parallel.MulticastReducer``)."""
+    if accumulate not in _ACC_MODES:
+        raise ValueError(f"unknown accumulate mode {accumulate!r}")
+    acc = _ACC_MODES[accumulate]
+    if acc != _lib.Q2_ACC_STORE and (out is None or out.dtype != torch.float32):
+        raise ValueError("accumulating GEMMs need a float32 `out`")
+    if (acc == _lib.Q2_ACC_MULTIMEM) != bool(multicast_ptr):
+        raise ValueError("multicast_ptr is required by, and only by, accumulate='multimem'")
     if qa.K != qb.K:
         raise ValueError(f"inner dimensions disagree: {qa.shape} vs {qb.shape}")
     M, N = qa.R, qb.R
@@ -172,8 +189,9 @@ def gemm(qa: NVFP4Tensor, qb: NVFP4Tensor, out_dtype=torch.float32, out: torch.T
     dt = _lib.Q2_F32 if out.dtype == torch.float32 else _lib.Q2_BF16
     a, b = qa.c(), qb.c()
     with torch.cuda.device(qa.device), torch.cuda.nvtx.range("q2.gemm"):
-        _lib.check(_lib.lib().q2_gemm_tn(ctypes.byref(a), ctypes.byref(b), out.data_ptr(), dt, out.stride(0),
-                                         int(accumulate), stream_handle()), "gemm")
+        dst = multicast_ptr if acc == _lib.Q2_ACC_MULTIMEM else out.data_ptr()
+        _lib.check(_lib.lib().q2_gemm_tn(ctypes.byref(a), ctypes.byref(b), dst, dt, out.stride(0),
+                                         acc, stream_handle()), "gemm")
     return out
 
 
@@ -262,9 +280,16 @@ def forward(x, w, cfg: LayerConfig = LayerConfig(), accumulate: str = "f32", out
 
 @api
 def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_dtype=torch.float32,
-             err=None, operands: dict | None = None) -> GradPair:
+             err=None, operands: dict | None = None, dw_out: torch.Tensor | None = None,
+             dw_accumulate="store", dw_multicast_ptr: int = 0) -> GradPair:
     """Backward from the tape and the output gradient (linear_graph.py:277-333).
 
+    ``dw_out`` / ``dw_accumulate`` / ``dw_multicast_ptr``: the wgrad GEMM writes into a
+    caller-owned fp32 [out, in] buffer with ``gemm``'s accumulate modes ("store", "add",
+    "red", or "multimem": dW summed over the data-parallel ranks inside the GEMM epilogue
+    through the buffer's NVLS multicast address, ``parallel.MulticastReducer``).  The
+    returned ``dW`` is then ``dw_out`` (complete only after the caller's cross-rank barrier
+    in the "multimem" case).
     ``operands``: optional dict that receives the four quantized GEMM operands the call
     computed ("E", "Wt" for dX; "Et", "Xt" for dW; None where an operand stays dense),
     for parity checks of the exact tensors the GEMMs consumed."""
@@ -275,6 +300,10 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     if es != (tokens, out_dim):
         raise ValueError(f"E has shape {es}, expected {(tokens, out_dim)}")
     mode = "posthoc" if cfg.posthoc else "exact"
+    if dw_out is not None and (dw_out.dtype != torch.float32 or tuple(dw_out.shape) != (out_dim, in_dim)):
+        raise ValueError(f"dw_out must be a float32 {(out_dim, in_dim)} tensor")
+    if dw_accumulate not in ("store", "add", "red", "multimem") or (dw_accumulate != "store" and dw_out is None):
+        raise ValueError(f"dw_accumulate={dw_accumulate!r} needs dw_out (store/add/red/multimem)")
     if accumulate not in ("f32", "f64"):
         raise ValueError(f"unknown accumulate precision {accumulate!r}")
     f64 = accumulate == "f64"                         # float64 products (the reference's oracle mode)
@@ -283,7 +312,12 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
     dense = lambda t: _dense64(t).to(wide)            # noqa: E731
     if cfg.backward_scheme == "identity":             # no backward quantization (linear_graph.py:286-288)
         ef = e2.to(wide)
-        return GradPair(torch.matmul(ef, dense(tape.qW)).to(dx_dtype), torch.matmul(ef.t(), dense(tape.qX)))
+        dw = torch.matmul(ef.t(), dense(tape.qX))
+        if dw_out is not None:
+            if dw_accumulate == "multimem":
+                raise ValueError("the multicast dW reduction needs both wgrad operands in NVFP4 (f32 accumulate)")
+            dw = dw_out.add_(dw) if dw_accumulate in ("add", "red") else dw_out.copy_(dw)
+        return GradPair(torch.matmul(ef, dense(tape.qW)).to(dx_dtype), dw)
     own = err is None
     if own:
         err = _err_word(e2.device)
@@ -313,6 +347,20 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
         b = dense(qb) if qb is not None else b_dense()
         return torch.matmul(a, b.t()).to(out_dtype)
 
+    def wprod(qa, qb, a_dense, b_dense):
+        """The wgrad product, into ``dw_out`` with its accumulate mode when one is given."""
+        if dw_out is None:
+            return product(qa, qb, a_dense, b_dense, wide)
+        if qa is not None and qb is not None and not f64:
+            return gemm(qa, qb, torch.float32, out=dw_out, accumulate=dw_accumulate,
+                        multicast_ptr=dw_multicast_ptr)
+        if dw_accumulate == "multimem":
+            raise ValueError("the multicast dW reduction needs both wgrad operands in NVFP4 (f32 accumulate)")
+        a = dense(qa) if qa is not None else a_dense()
+        b = dense(qb) if qb is not None else b_dense()
+        r = torch.matmul(a.float(), b.float().t())
+        return dw_out.add_(r) if dw_accumulate in ("add", "red") else dw_out.copy_(r)
+
     # MS-EDEN of E for both GEMMs from one read of E (tensor-core dual kernel) when E is a
     # bf16 [tokens, out] with both dims multiples of 128; identical results to two msed calls
     dual = (not sr_scheme and q_e and q_w and q_et and q_xt and e2.dtype == torch.bfloat16
@@ -328,7 +376,7 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
             qxt = quant(tape.qX, PAIR_DW, 1, "cols" if isinstance(tape.qX, torch.Tensor) else "tape", True)
             side.wait_event(e_done)
             qet = qet_d
-            dw = product(qet, qxt, None, None, wide)
+            dw = wprod(qet, qxt, None, None)
             _keep(side, qet_d)                           # made on the caller's stream, read here
         elif (q_et or q_xt) if sr_scheme else (q_et and q_xt):
             both = q_et and q_xt
@@ -339,10 +387,8 @@ def backward(tape: LinearTape, e, seeds: SeedPair, accumulate: str = "f32", dx_d
             qet = qxt = None
         if dual:
             pass
-        elif qet is None and qxt is None:
-            dw = torch.matmul(e2.to(wide).t(), dense(tape.qX))
         else:
-            dw = product(qet, qxt, lambda: e2.to(wide).t(), lambda: dense(tape.qX).t(), wide)
+            dw = wprod(qet, qxt, lambda: e2.to(wide).t(), lambda: dense(tape.qX).t())
     # dX = Q(E) Q(W^T)^T, inner dimension = out features
     qw = tape.qW.rows if isinstance(tape.qW, SquareBlockTensor) else tape.qW
     qe = qwt = None

@@ -118,3 +118,19 @@ def test_weak_scaling_bookkeeping(world):
     per_gpu = bench.flops(bench.TOKENS)
     assert per_gpu == sum(6.0 * bench.TOKENS * i * o for _, i, o in bench.PROJECTIONS)
     assert bench.TOKENS % 128 == 0 and (65536 // max(world, 1)) % 128 == 0
+
+
+def test_reducer_layout():
+    from paper_2601_22813_b200.parallel import reducer_layout
+    offs, n = reducer_layout([(6144, 2048), (2048, 2048), (3, 5)])
+    assert offs == [0, 6144 * 2048, 6144 * 2048 + 2048 * 2048]
+    assert n == offs[-1] + 64 and all(o % 64 == 0 for o in offs)
+    with pytest.raises(ValueError):
+        reducer_layout([(0, 4)])
+
+
+def test_sharded_step_rejects_unknown_reduce():
+    from paper_2601_22813_b200.parallel import ShardedLinearStep
+    s = ShardedLinearStep(linear_fwd=lambda X, W: (X, None), linear_bwd=lambda t, E, s: (E, E), reduce="bogus")
+    with pytest.raises(ValueError):
+        s.step([(1, 2, 3)], 0)
