@@ -61,7 +61,7 @@ constexpr int TC_NRAW = 3;
 constexpr int TC_META = 4;                       // metadata ring (tile flags)
 constexpr int TC_META_BYTES = 320;               // words: [0] flags, [1..4] rows z0 mask, [5..8] cols z0 mask, [9] tile max
                                                  // bits; bytes 64..191 small count per row chunk, 192..319 per column chunk
-constexpr int TC_DEF_CAP = 256;
+constexpr int TC_DEF_CAP = 4096;                 // deferred chunks per CTA before the epilogue must settle them inline
 constexpr int TC_PF = 6;                         // tiles prefetched into L2 ahead of the TMA ring
 // Shared memory: B operands diag(s) H per orientation (32 KB each) | NS stages of main + small (64 KB each) | tape raw ring |
 // metadata ring | deferred list | misc | barriers.  bf16 sources: 3 stages
