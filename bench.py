@@ -215,9 +215,10 @@ def main():
     ap.add_argument("--mode", default="posthoc", choices=["posthoc", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the c1 / c2 / c5 configs")
-    ap.add_argument("--dw-reduce", default="auto", choices=["auto", "nccl", "multimem"],
+    ap.add_argument("--dw-reduce", default="nccl", choices=["auto", "nccl", "multimem"],
                     help="N > 1: dW sum by NCCL all-reduce or inside the wgrad GEMM over NVLS multicast "
-                         "(auto: multimem when the group has a multicast object)")
+                         "(auto: multimem when the group has a multicast object).  Default nccl: the "
+                         "multicast path has not run on a multi-GPU box yet (every box this round had one GPU)")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of the captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
