@@ -183,6 +183,32 @@ def _time_ms(fn, iters=5, warmup=2):
     return s.elapsed_time(e) / iters
 
 
+def _graph_ms(fn, iters=10):
+    """Mean device time of fn() with the calls captured in one CUDA graph (no host launch
+    overhead: the small c2 sizes were host-bound when timed eagerly); eager on failure."""
+    import torch
+    try:
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(iters):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        s, e = _events()
+        s.record()
+        g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / iters
+        del g
+        return ms, "cuda_graph"
+    except Exception as exc:  # noqa: BLE001 - report and fall back
+        torch.cuda.synchronize()
+        return _time_ms(fn, iters=3, warmup=1), f"eager ({type(exc).__name__})"
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -511,9 +537,12 @@ def extra_configs(q2, args, dev):
     c1 = {}
     for mode in ("posthoc", "exact"):
         cfg = q2.LayerConfig(posthoc=mode == "posthoc")
-        c1[mode + "_ms"] = _time_ms(lambda: q2.backward(q2.forward(X, W, cfg, out_dtype=torch.bfloat16)[1], E, seeds,
-                                                        dx_dtype=torch.bfloat16), iters=20, warmup=3)
+        layer = lambda: q2.backward(q2.forward(X, W, cfg, out_dtype=torch.bfloat16)[1], E, seeds,  # noqa: E731
+                                    dx_dtype=torch.bfloat16)
+        c1[mode + "_ms"] = _time_ms(layer, iters=20, warmup=3)
+        c1[mode + "_graph_ms"], _ = _graph_ms(layer, iters=20)
     c1["bf16_ms"] = _time_ms(lambda: (X @ W.t(), E @ W, E.t() @ X), iters=20, warmup=3)
+    c1["bf16_graph_ms"], _ = _graph_ms(lambda: (X @ W.t(), E @ W, E.t() @ X), iters=20)
     f1 = 6.0 * 2048 * 1024 * 1024
     x64, w64, e64 = (t.double().cpu().numpy() for t in (X, W, E))
     t0 = time.perf_counter()
@@ -522,7 +551,7 @@ def extra_configs(q2, args, dev):
     c1["oracle_ms"] = (time.perf_counter() - t0) * 1e3
     c1["oracle_cores"] = _threads()
     c1["TFLOP/s"] = {k: f1 / (v / 1e3) / 1e12 for k, v in c1.items() if k.endswith("_ms")}
-    out["c1"] = dict(c1, workload="1024->1024, 2048 tokens, fwd+bwd (eager launches)")
+    out["c1"] = dict(c1, workload="1024->1024, 2048 tokens, fwd+bwd (*_ms: eager launches from Python; *_graph_ms: 20 layer calls captured in one CUDA graph)")
 
     # c2: quantizer sweep, [N/4096, 4096] bf16 ~ N(0,1) x LogNormal(0,1) per row
     c2 = {}
@@ -534,9 +563,9 @@ def extra_configs(q2, args, dev):
                              ("msed_rows", lambda: q2.msed(x, seeds, 6.0, 1, 2, args.mode, "rows"), 2.5625),
                              ("msed_cols", lambda: q2.msed(x, seeds, 6.0, 3, 4, args.mode, "cols"), 2.5625),
                              ("msed_dual", lambda: q2.msed_dual(x, seeds, 1, 2, 3, 4, 6.0, args.mode), 3.125)):
-            ms = _time_ms(fn, iters=3, warmup=1)
+            ms, how = _graph_ms(fn, iters=10 if lg <= 26 else 3)
             gbs = n * bpe / (ms / 1e3) / 1e9
-            r[tag] = {"ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm}
+            r[tag] = {"ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm, "timing": how}
         if lg == 24:
             # the reference's algorithm on the host cores (oracle port), same tensor, one call each
             x64 = x.double().cpu().numpy()
