@@ -134,3 +134,50 @@ def test_sharded_step_rejects_unknown_reduce():
     s = ShardedLinearStep(linear_fwd=lambda X, W: (X, None), linear_bwd=lambda t, E, s: (E, E), reduce="bogus")
     with pytest.raises(ValueError):
         s.step([(1, 2, 3)], 0)
+
+
+class _FakeReducer:
+    """Stands in for MulticastReducer on CPU: records the protocol calls."""
+
+    def __init__(self, shapes):
+        from paper_2601_22813_b200.parallel import reducer_layout
+        self.shapes = [tuple(s) for s in shapes]
+        self.offsets, _ = reducer_layout(self.shapes)
+        self.mc_base = 1 << 40
+        self.log = []
+        import numpy as np
+        self.views = [np.zeros(sh) for sh in self.shapes]
+
+    def target(self, i):
+        from paper_2601_22813_b200.parallel import MulticastReducer
+        return MulticastReducer.target(self, i)          # the real address arithmetic
+
+    def begin(self):
+        self.log.append("begin")
+
+    def finish(self):
+        self.log.append("finish")
+
+
+def test_sharded_step_multimem_protocol():
+    """reduce="multimem": one begin() before the first wgrad, every backward gets its
+    projection's dW slot and multicast address (base + 4 B x float offset), one finish()
+    after the last, and no NCCL all-reduce is issued."""
+    from paper_2601_22813_b200.parallel import ShardedLinearStep
+    calls = []
+
+    def bwd(tape, E, seeds, **kw):
+        calls.append(kw)
+        return E, kw["dw_out"]
+
+    shapes = [(384, 256), (256, 256)]
+    red = _FakeReducer(shapes)
+    s = ShardedLinearStep(linear_fwd=lambda X, W: (X, None), linear_bwd=bwd, rank=0, world=2,
+                          reduce="multimem", reducer=red)
+    W = [type("W", (), {"shape": sh, "device": "cpu"})() for sh in shapes]
+    out = s.step([(1, W[0], 2), (1, W[1], 3)], 0)
+    assert red.log == ["begin", "finish"]
+    assert [c["dw_accumulate"] for c in calls] == ["multimem", "multimem"]
+    assert calls[0]["dw_multicast_ptr"] == (1 << 40)
+    assert calls[1]["dw_multicast_ptr"] == (1 << 40) + 4 * 384 * 256
+    assert out[1][2].shape == (256, 256)
