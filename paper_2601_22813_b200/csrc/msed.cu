@@ -211,6 +211,17 @@ static int tc_run(int src, TcArgs& a, int mode, cudaStream_t st) {
   int rc;
   if (mode == Q2_MSED_POSTHOC) {
     if ((rc = dispatch_tc<TC_POSTHOC>(src, a, 0, st))) return rc;
+    static const bool split2 = getenv("Q2_PASS2_SPLIT") != nullptr;   // A/B: one pass-2 launch per orientation
+    if (src == TC_DUAL && !split2 && (a.o[0].R + 255) / 256 < 65535 && (a.o[1].R + 255) / 256 < 65535) {
+      Pass2Op p[2];
+      for (int o = 0; o < 2; ++o)
+        p[o] = Pass2Op{(const uint16_t*)a.o[o].aw, (const unsigned long long*)a.o[o].red, (uint32_t)a.o[o].R,
+                       (uint32_t)a.o[o].K, a.o[o].sf, a.o[o].scale32};
+      const int64_t gx = std::max((((a.o[0].K + 63) / 64) + 3) / 4, (((a.o[1].K + 63) / 64) + 3) / 4);
+      const int64_t gy = std::max((a.o[0].R + 255) / 256, (a.o[1].R + 255) / 256);
+      return launch_pdl(tc_pass2t_dual_kernel, dim3((unsigned)gx, (unsigned)gy, 2), dim3(256), 0, st, p[0], p[1],
+                        a.err) == cudaSuccess ? Q2_OK : Q2_ECUDA;
+    }
     for (int o = 0; o < 2; ++o)
       if ((src >> o) & 1)
         if ((rc = tc_pass2(a.o[o], a.err, st))) return rc;

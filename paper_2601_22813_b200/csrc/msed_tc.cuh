@@ -1206,20 +1206,22 @@ __global__ void __launch_bounds__(256) tc_pass2_kernel(const uint16_t* __restric
 // (normal range: one shift-add of the word, aword_code otherwise), places them at their
 // position in the scale layout in shared memory, and the block writes its 4 KiB of
 // scales contiguously (rows past R get scale 0: deterministic padding).
-__global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restrict__ aw,
-                                                        const unsigned long long* __restrict__ red, uint32_t R,
-                                                        uint32_t K, uint8_t* __restrict__ sf,
-                                                        float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
-  __shared__ __align__(16) uint32_t tile[4 * 256];
-  pdl_trigger();
-  pdl_wait();
+struct Pass2Op {
+  const uint16_t* aw; const unsigned long long* red; uint32_t R, K; uint8_t* sf; float* scale32_out;
+};
+
+// Post-hoc pass 2 of one operand: block (bx, by) covers rows 256 by .. and scale blocks 4 bx ..
+__device__ __forceinline__ void pass2t_body(const uint16_t* __restrict__ aw, const unsigned long long* __restrict__ red,
+                                            uint32_t R, uint32_t K, uint8_t* __restrict__ sf,
+                                            float* __restrict__ scale32_out, uint32_t* __restrict__ err,
+                                            uint32_t bx, uint32_t by, uint32_t (&tile)[4 * 256]) {
   const uint64_t pb = red[1];
   const double pmax = __longlong_as_double((long long)pb);
   const int E = (int)(pb >> 52) - 1023;
   const int k = (pb & ((1ull << 52) - 1)) == 0 ? E - 8 : E - 7;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
-  const uint32_t kb = (K + 63) / 64, jb0 = 4 * blockIdx.x, nj = min(4u, kb - jb0);
-  const uint32_t t = threadIdx.x, r = 256 * blockIdx.y + t;
+  if (bx == 0 && by == 0 && threadIdx.x == 0) *scale32_out = pmax > 0.0 ? (float)ldexp(1.0, k) : 0.f;
+  const uint32_t kb = (K + 63) / 64, jb0 = 4 * bx, nj = min(4u, kb - jb0);
+  const uint32_t t = threadIdx.x, r = 256 * by + t;
   // word of row t within a 1 KiB block: byte (L/8)*256 + h*128 + (L%8)*16 + c*4, row = 128h + 32c + L
   const uint32_t L = t & 31, c = (t >> 5) & 3, h = t >> 7;
   const uint32_t widx = (L >> 3) * 64 + h * 32 + (L & 7) * 4 + c;
@@ -1237,9 +1239,32 @@ __global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restri
   }
   if (ovf) atomic_or_err(err, Q2_ERR_SCALE448);
   __syncthreads();
-  uint4* dst = reinterpret_cast<uint4*>(sf + (((uint64_t)blockIdx.y * kb + jb0) << 10));
+  uint4* dst = reinterpret_cast<uint4*>(sf + (((uint64_t)by * kb + jb0) << 10));
   const uint4* src = reinterpret_cast<const uint4*>(tile);
   for (uint32_t i = t; i < nj * 64; i += 256) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restrict__ aw,
+                                                        const unsigned long long* __restrict__ red, uint32_t R,
+                                                        uint32_t K, uint8_t* __restrict__ sf,
+                                                        float* __restrict__ scale32_out, uint32_t* __restrict__ err) {
+  __shared__ __align__(16) uint32_t tile[4 * 256];
+  pdl_trigger();
+  pdl_wait();
+  pass2t_body(aw, red, R, K, sf, scale32_out, err, blockIdx.x, blockIdx.y, tile);
+}
+
+// Both orientations of a dual post-hoc call in one launch: block z = orientation; blocks
+// outside an operand's (scale blocks / 4) x (rows / 256) grid exit (one launch and one tail
+// instead of two).
+__global__ void __launch_bounds__(256) tc_pass2t_dual_kernel(Pass2Op o0, Pass2Op o1, uint32_t* __restrict__ err) {
+  __shared__ __align__(16) uint32_t tile[4 * 256];
+  pdl_trigger();
+  pdl_wait();
+  const Pass2Op& o = blockIdx.z ? o1 : o0;
+  const uint32_t gx = ((o.K + 63) / 64 + 3) / 4, gy = (o.R + 255) / 256;
+  if (blockIdx.x >= gx || blockIdx.y >= gy) return;
+  pass2t_body(o.aw, o.red, o.R, o.K, o.sf, o.scale32_out, err, blockIdx.x, blockIdx.y, tile);
 }
 
 }  // namespace q2
