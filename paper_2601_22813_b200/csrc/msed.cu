@@ -217,10 +217,11 @@ static int tc_run(int src, TcArgs& a, int mode, cudaStream_t st) {
       for (int o = 0; o < 2; ++o)
         p[o] = Pass2Op{(const uint16_t*)a.o[o].aw, (const unsigned long long*)a.o[o].red, (uint32_t)a.o[o].R,
                        (uint32_t)a.o[o].K, a.o[o].sf, a.o[o].scale32};
-      const int64_t gx = std::max((((a.o[0].K + 63) / 64) + 3) / 4, (((a.o[1].K + 63) / 64) + 3) / 4);
-      const int64_t gy = std::max((a.o[0].R + 255) / 256, (a.o[1].R + 255) / 256);
-      return launch_pdl(tc_pass2t_dual_kernel, dim3((unsigned)gx, (unsigned)gy, 2), dim3(256), 0, st, p[0], p[1],
-                        a.err) == cudaSuccess ? Q2_OK : Q2_ECUDA;
+      int64_t nb = 0;
+      for (int o = 0; o < 2; ++o) nb += ((((a.o[o].K + 63) / 64) + 3) / 4) * ((a.o[o].R + 255) / 256);
+      if (nb < (1ll << 31))
+        return launch_pdl(tc_pass2t_dual_kernel, dim3((unsigned)nb), dim3(256), 0, st, p[0], p[1],
+                          a.err) == cudaSuccess ? Q2_OK : Q2_ECUDA;
     }
     for (int o = 0; o < 2; ++o)
       if ((src >> o) & 1)

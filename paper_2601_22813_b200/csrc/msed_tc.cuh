@@ -1254,17 +1254,20 @@ __global__ void __launch_bounds__(256) tc_pass2t_kernel(const uint16_t* __restri
   pass2t_body(aw, red, R, K, sf, scale32_out, err, blockIdx.x, blockIdx.y, tile);
 }
 
-// Both orientations of a dual post-hoc call in one launch: block z = orientation; blocks
-// outside an operand's (scale blocks / 4) x (rows / 256) grid exit (one launch and one tail
-// instead of two).
+// Both orientations of a dual post-hoc call in one launch (one launch and one tail instead
+// of two): a 1-D grid, the first gx0 * gy0 blocks cover operand 0's (scale blocks / 4) x
+// (rows / 256) grid, the rest operand 1's (the two grids are transposes of each other, so a
+// 2-D grid of their maxima would be mostly empty blocks for skinny shapes).
 __global__ void __launch_bounds__(256) tc_pass2t_dual_kernel(Pass2Op o0, Pass2Op o1, uint32_t* __restrict__ err) {
   __shared__ __align__(16) uint32_t tile[4 * 256];
   pdl_trigger();
   pdl_wait();
-  const Pass2Op& o = blockIdx.z ? o1 : o0;
-  const uint32_t gx = ((o.K + 63) / 64 + 3) / 4, gy = (o.R + 255) / 256;
-  if (blockIdx.x >= gx || blockIdx.y >= gy) return;
-  pass2t_body(o.aw, o.red, o.R, o.K, o.sf, o.scale32_out, err, blockIdx.x, blockIdx.y, tile);
+  const uint32_t gx0 = ((o0.K + 63) / 64 + 3) / 4, n0 = gx0 * ((o0.R + 255) / 256);
+  const bool second = blockIdx.x >= n0;
+  const Pass2Op& o = second ? o1 : o0;
+  const uint32_t gx = second ? ((o1.K + 63) / 64 + 3) / 4 : gx0;
+  const uint32_t b = second ? blockIdx.x - n0 : blockIdx.x;
+  pass2t_body(o.aw, o.red, o.R, o.K, o.sf, o.scale32_out, err, b % gx, b / gx, tile);
 }
 
 }  // namespace q2
